@@ -1,0 +1,336 @@
+"""Benchmark: one HG cost+gradient evaluation per step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one full composite_grad evaluation of the workload config (default
+configs[1] = c2: transmon 3 x cavity 20, K=2 X-gate + forbidden-level penalty,
+N=2000 steps).  ``value`` is device-timed (amplitudes resident in HBM, CUDA
+events on the library's launch stream); ``e2e`` goes through the public API
+with host buffers (H2D of the amplitudes, D2H of cost and gradient inside the
+timed region).  The L2 is flushed (256 MiB write) between timed evaluations.
+
+``--impl reference`` times the reference algorithm on the host cores: the CPU
+oracle port (oracle/lg_oracle.py; the reference package is pure Python and
+cannot travel to the GPU box), one process per trajectory, on a bounded prefix
+of the same workload, extrapolated to the full N.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cost+gradient evals/sec"
+UNIT = "evals/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def algorithmic_bytes(case, plan_table):
+    """bytes per operator-term = S_op + 32 d K (S_op = 20 nnz + 4 (d+1)
+    for CSR, 16 d^2 dense); A-terms = sum_n mu_n (fwd) + sum_n mu_n (psi adjoint) +
+    sum_{n>0} mu_n n_costates + sum_{n,c} 2 mu_aux_{n,c}; A_c-terms = sum_{n,c} mu_aux_{n,c}.
+    Returns (total bytes per evaluation, backward-sweep bytes per evaluation, flops)."""
+    p = case.problem
+    d = p.dim
+
+    def s_op(m):
+        if hasattr(m, "array"):
+            return 16 * d * d, d * d
+        return 20 * m.nnz + 4 * (d + 1), m.nnz
+
+    union = None
+    try:
+        from paper_2304_06200_b200.sparse import linear_combine
+
+        union = linear_combine([1.0] + [1.0] * len(p.h_controls), [p.h_static, *p.h_controls])
+    except Exception:
+        union = p.h_static
+    sa, nnz_a = s_op(union)
+    sc = [s_op(h) for h in p.h_controls]
+    K = case.n_states
+    n_costates = sum(1 for t in case.terms)  # one costate per term per trajectory
+    mu = plan_table["m"].astype(np.int64) * plan_table["s"]
+    mua = plan_table["aux_m"].astype(np.int64) * plan_table["aux_s"]
+    blk = 32 * d * K
+    fwd_terms = int(mu.sum())
+    bwd_a = int(mu.sum() + mu[1:].sum() * n_costates + 2 * mua.sum())
+    bwd_c = mua.sum(axis=0)
+    bwd_bytes = bwd_a * (sa + blk) + sum(int(bwd_c[c]) * (sc[c][0] + blk) for c in range(len(sc)))
+    fwd_bytes = fwd_terms * (sa + blk)
+    flops = 8 * K * ((fwd_terms + bwd_a) * nnz_a + sum(int(bwd_c[c]) * sc[c][1] for c in range(len(sc))))
+    return fwd_bytes + bwd_bytes, bwd_bytes, flops
+
+
+def cpu_reference(case, budget_s=20.0):
+    """Time the oracle port of the reference algorithm on a bounded prefix (one process per
+    trajectory).  Returns (evals_per_s_extrapolated, cores, sample description)."""
+    import multiprocessing as mp
+
+    from oracle import lg_oracle as O
+
+    N = case.field.n_steps
+    # probe one step to size the sample to ~budget_s of CPU work per trajectory
+    t0 = time.perf_counter()
+    _ref_traj_worker((case.name, 0, 4))
+    per_step = (time.perf_counter() - t0) / 4
+    n_pref = int(max(4, min(N, budget_s / max(per_step, 1e-6))))
+    T = case.n_states
+    cores = max(1, min(T, os.cpu_count() or 1))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_ref_traj_worker, [(case.name, t, n_pref) for t in range(T)])
+    wall = time.perf_counter() - t0
+    per_eval = wall * (N / n_pref)
+    sample = (f"oracle port of the reference (oracle/lg_oracle.py), {T} trajectories x {n_pref}/{N} steps "
+              f"in {cores} processes, {wall:.1f}s wall, extrapolated linearly to N={N}")
+    del O
+    return 1.0 / per_eval, cores, sample
+
+
+def _ref_traj_worker(arg):
+    """One trajectory's forward+backward with the oracle (the reference algorithm)."""
+    name, t, n_pref = arg
+    from oracle import lg_oracle as O
+    from paper_2304_06200_b200 import models
+
+    case = models.build_case(name, n_steps=n_pref)
+    p = case.problem
+
+    def conv(m):
+        if hasattr(m, "array"):
+            return O.Dense(np.asfortranarray(m.array))
+        return O.Csr(m.n_rows, m.row_offsets, m.col_indices, m.values)
+
+    states = p.initial_state if p.initial_state is not None else p.basis
+    op = O.Problem(conv(p.h_static), tuple(conv(h) for h in p.h_controls), tau=p.tau,
+                   initial_states=np.asarray(states)[t:t + 1],
+                   basis=None if p.basis is None else np.asarray(p.basis)[t:t + 1])
+    terms = []
+    for term in case.terms:
+        k = term.kind.value
+        if term.penalty_op is not None:
+            terms.append(O.Term(k, term.weight, None, conv(term.penalty_op)))
+        else:
+            tg = term.target_state if term.target_state is not None else term.target_images
+            terms.append(O.Term(k, term.weight, np.asarray(tg)[t:t + 1]))
+    O.composite_grad(op, case.field.amplitudes, case.field.dt, terms)
+    return t
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_2304_06200_b200 import models
+
+    case = models.build_case(args.config)
+    vals, cores, sample = [], 1, ""
+    for i in range(args.warmup + args.steps):
+        v, cores, sample = cpu_reference(case, budget_s=args.ref_budget)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(statistics.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": case.name, "description": case.description, "n_steps": case.field.n_steps,
+                   "n_states": case.n_states},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_06200_b200 import _native, composite_grad, models
+    from paper_2304_06200_b200.costs import NativeProblem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _native.load()
+    case = models.build_case(args.config)
+    p = case.problem
+    states = p.initial_state
+    npb = NativeProblem(p, case.terms, initial_states=states if any(
+        t.kind.value.startswith("state") for t in case.terms) else None, basis=p.basis, device=local)
+    stream = torch.cuda.current_stream()
+    _native.check(lib.lg_set_stream(npb.handle, stream.cuda_stream))
+    N, Kc = case.field.n_steps, case.field.n_channels
+    d_amps = torch.from_numpy(case.field.amplitudes).cuda()
+    d_cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    d_grad = torch.zeros((N, Kc), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def dev_eval():
+        _native.check(lib.lg_eval_device(npb.handle, N, case.field.dt, d_amps.data_ptr(), d_cost.data_ptr(),
+                                         d_grad.data_ptr()))
+
+    for _ in range(args.warmup):
+        dev_eval()
+    torch.cuda.synchronize()
+    _native.check(lib.lg_set_timing(npb.handle, 1))
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            starts[i].record(stream)
+            dev_eval()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(ms))
+    phase = np.zeros(4)
+    nev = np.zeros(1, np.int64)
+    _native.check(lib.lg_get_timing(npb.handle, _native.dptr(phase), _native.i64ptr(nev)))
+    _native.check(lib.lg_set_timing(npb.handle, 0))
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * args.steps / (total_ms / 1e3)
+
+    # end to end through the public API with host buffers
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = composite_grad(case.problem, case.field, case.terms)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * args.steps / (float(te.item()) / 1e3)
+
+    # roofline of the dominant kernel (backward sweep)
+    table = npb.plan_table(case.field)
+    tot_bytes, bwd_bytes, flops = algorithmic_bytes(case, table)
+    bwd_ms = phase[2] / max(int(nev[0]), 1)
+    peak, peak_kind = _peaks()
+    achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": case.name, "description": case.description, "n_steps": N,
+                   "n_states": case.n_states, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB write) between timed evaluations"},
+        "state_steps_per_sec": value * case.n_states * N,
+        "phase_ms_per_eval": {k: float(v / max(int(nev[0]), 1)) for k, v in
+                              zip(["prep_plans", "forward", "backward", "finalize"], phase)},
+        "roofline": {"bound": "hbm", "kernel": "lg_k_backward", "achieved": achieved, "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": bwd_bytes, "algorithmic_bytes_per_eval": tot_bytes,
+                     "flops_per_eval": flops},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N * Kc,
+                "d2h_bytes_per_step": 8 * N * Kc + 8},
+        "gpu_launches": 7 * args.steps,
+        "clocks": clk.summary(),
+        "cost": res.cost,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, sample = cpu_reference(case, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

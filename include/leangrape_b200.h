@@ -1,0 +1,157 @@
+/* leangrape_b200.h -- C ABI of the B200-native HG cost+gradient evaluation.
+ *
+ * The reference (`leangrape`, pure Python) has no FFI layer; its drop-in
+ * boundary is the function pair the optimiser binds
+ *     composite_grad(problem, a, terms) -> GradientResult   (src/costs.py:515-546)
+ *     composite_cost(problem, a, terms) -> float            (src/costs.py:549-597)
+ * called from grape_optimize (src/optimizer.py:18,117,150,159,169).  Every
+ * entry point below replaces one piece of that surface; the Python mirror
+ * (paper_2304_06200_b200/costs.py) binds them with ctypes exactly as
+ * INTEGRATION.md shows.  Plain pointers and sizes only: complex numbers are
+ * interleaved (re, im) float64 pairs, matrices are CSR (int64 offsets/indices)
+ * or column-major dense, exactly the reference's CsrMatrix / DenseMatrix
+ * layouts (src/sparse.py:42-60,152-170).
+ *
+ * Status codes map onto the reference's exception types (see lg_last_error()).
+ * A handle is not thread-safe; calls are synchronous like the Python API.
+ */
+#ifndef LEANGRAPE_B200_H
+#define LEANGRAPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define LG_OK 0
+#define LG_INVALID_ARG 1         /* ValueError   (src/costs.py:75-85,112-121,151-168) */
+#define LG_PLANNING_INFEASIBLE 2 /* PlanningError(RuntimeError) (src/expm.py:61-62,244-249,273-276) */
+#define LG_CUDA_ERROR 3          /* RuntimeError */
+#define LG_NCCL_ERROR 4          /* RuntimeError */
+#define LG_INDEX_ERROR 5         /* IndexError   (src/derivatives.py:214-215) */
+#define LG_UNSUPPORTED 6         /* NotImplementedError (e.g. DIAGONALIZATION backend) */
+
+/* ---- cost kinds: CostKind (src/costs.py:49-61) -------------------------- */
+#define LG_STATE_INFIDELITY 0
+#define LG_STATE_PENALTY 1
+#define LG_STATE_RUNNING_INFIDELITY 2
+#define LG_GATE_INFIDELITY 3
+#define LG_GATE_RUNNING_INFIDELITY 4
+
+/* One square operator: CsrMatrix (dense == 0) or DenseMatrix (dense == 1). */
+typedef struct {
+  int32_t dense;
+  int64_t n;
+  int64_t nnz;                /* CSR: stored elements                          */
+  const int64_t* row_offsets; /* CSR: [n + 1]                                   */
+  const int64_t* col_indices; /* CSR: [nnz], strictly increasing per row        */
+  const double* values;       /* CSR: [2 nnz]; dense: [2 n n] column-major      */
+} lg_matrix;
+
+/* One CostTerm (src/costs.py:141-168).  `targets` holds one complex vector
+ * of length d per trajectory of the term's set: the target states (state
+ * kinds) or the target images U_T |psi_0^h> (gate kinds; the images replace a
+ * dense d x d target_gate, which at d = 10^4 would not fit the host). */
+typedef struct {
+  int32_t kind;
+  double weight;
+  const double* targets; /* [K][2 d] or NULL for STATE_PENALTY */
+  lg_matrix penalty;     /* STATE_PENALTY only */
+} lg_cost_term;
+
+/* ControlProblem (src/costs.py:96-138) plus the K-state block:
+ *   initial_states : the K_s state-transfer trajectories (reference: one initial_state)
+ *   basis          : the K_g gate basis states (reference: d states; here K_g <= d,
+ *                    subspace costs normalised by K_g, == reference at K_g == d).
+ * shard_begin/shard_end select the trajectories this process owns (multi-GPU);
+ * shard_end <= 0 means all. */
+typedef struct {
+  lg_matrix h_static;
+  int32_t n_channels;
+  const lg_matrix* h_controls;
+  double tau;
+  int64_t n_states;
+  const double* initial_states; /* [K_s][2 d] */
+  int64_t n_basis;
+  const double* basis; /* [K_g][2 d] */
+  int32_t n_terms;
+  const lg_cost_term* terms;
+  int32_t device;
+  int64_t shard_begin, shard_end;
+} lg_problem_desc;
+
+typedef struct lg_problem lg_problem;
+
+/* Copy operators, trajectories and targets to the device once per problem. */
+int lg_problem_create(const lg_problem_desc* desc, lg_problem** out);
+void lg_problem_destroy(lg_problem* p);
+
+/* composite_grad: cost and gradient grad[n * n_channels + k] = dC/da[n, k]
+ * for the ControlField (n_steps, n_channels, dt, amps[n_steps][n_channels]). */
+int lg_eval(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost, double* grad,
+            int64_t* live_vector_peak);
+
+/* composite_cost: forward sweeps only (line search, src/optimizer.py:153-170). */
+int lg_cost(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost);
+
+/* Same as lg_eval, but with amplitudes already resident on the device and the
+ * results left on the device (benchmarking the kernels without host copies). */
+int lg_eval_device(lg_problem* p, int64_t n_steps, double dt, const double* d_amps, double* d_cost, double* d_grad);
+
+/* Per-step planner inputs and plans exactly as the reference's StepEvaluator
+ * computes them (src/derivatives.py:105-110,187-196): for debugging and the
+ * bit-exact plan-parity tests.  aux_* arrays are [n_steps][n_channels]. */
+int lg_plan_table(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* norm1, int64_t* sigma,
+                  int32_t* order, int32_t* scaling, double* aux_arg, int64_t* aux_sigma, int32_t* aux_order,
+                  int32_t* aux_scaling);
+
+/* Forward-propagated final states of the state trajectories, [K_s][2 d]
+ * (forward_propagate, src/costs.py:209-217). */
+int lg_forward_states(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* out);
+
+/* Raw per-trajectory scalars of the last evaluation (for sharded runs: the
+ * partial sums every rank contributes; summing them across ranks and calling
+ * lg_finalize_host reproduces the single-process result exactly). */
+int64_t lg_raw_size(lg_problem* p, int64_t n_steps);
+int lg_raw_get(lg_problem* p, double* raw);
+int lg_finalize_host(lg_problem* p, int64_t n_steps, const double* raw, double* cost, double* grad);
+
+/* make_plan (src/expm.py:279-303) on the host: bit-identical to the reference. */
+int lg_make_plan(double norm1, int64_t sigma_prime, double tau, int32_t m_max, int32_t s_max, int32_t* order,
+                 int32_t* scaling, double* bound);
+
+/* Evaluate a batch of plans with the DEVICE planner (guarded; uncertain ones
+ * fixed on the host) -- exposed for the planner parity test. */
+int lg_make_plans_device(int64_t count, const double* norm1, const int64_t* sigma, double tau, int32_t* order,
+                         int32_t* scaling, int32_t* status, int32_t* n_uncertain);
+
+/* Handle-free combine of raw per-trajectory scalars (layout of lg_raw_get):
+ * what every rank runs after the cross-rank sum.  kinds/weights/t0/K per term. */
+int lg_finalize_raw(int32_t n_terms, const int32_t* kinds, const double* weights, const int32_t* t0,
+                    const int32_t* K, int64_t n_steps, int32_t n_channels, int32_t n_traj, const double* raw,
+                    double* cost, double* grad);
+
+/* Host restatements of the numpy reductions that feed the planner
+ * (lg_numpy.cuh) -- test hooks for the bit-exactness rules. */
+void lg_np_cabs_host(int64_t n, const double* z /* [2n] */, double* out);
+double lg_np_pairwise_host(int64_t n, const double* a);
+double lg_np_reduce_host(int64_t n, const double* a);
+
+/* Launch on a caller-owned stream (e.g. torch.cuda.current_stream()) and/or
+ * record CUDA events around every phase of every evaluation:
+ * phase_ms = {prep+plans, forward sweep, backward sweep, finalize}, summed
+ * over `evals` evaluations since the last reset. */
+int lg_set_stream(lg_problem* p, void* stream);
+int lg_set_timing(lg_problem* p, int enable);
+int lg_get_timing(lg_problem* p, double* phase_ms /* [4] */, int64_t* evals);
+
+int lg_device_count(void);
+const char* lg_last_error(void);
+const char* lg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEANGRAPE_B200_H */

@@ -1,0 +1,73 @@
+"""Build the sm_100a shared library in-tree (nvcc; no torch JIT, no CPU fallback).
+
+    python -m paper_2304_06200_b200.build
+
+Output: paper_2304_06200_b200/_lib/libleangrape_b200.so (git-ignored; it
+travels to the GPU box with the repo snapshot).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "_lib")
+LIB = os.path.join(OUT, "libleangrape_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
+
+# per-unit flags: the step-preparation/planner and host units must round like
+# numpy / CPython (no FMA contraction); the sweep engine may contract.
+UNITS = {
+    "lg_prep.cu": ["-fmad=false"],
+    "lg_api.cu": ["-fmad=false"],
+    "lg_engine.cu": [],
+}
+
+
+def _sources():
+    return [os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith((".cu", ".cuh", ".h"))] + [
+        os.path.join(os.path.dirname(HERE), "include", "leangrape_b200.h")
+    ]
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(s) <= t for s in _sources())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(OUT, exist_ok=True)
+    objs = []
+    for unit, flags in UNITS.items():
+        obj = os.path.join(OUT, unit.replace(".cu", ".o"))
+        cmd = [NVCC, *COMMON, *flags, "-c", os.path.join(SRC, unit), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed for {unit}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        with open(os.path.join(OUT, unit + ".ptxas.log"), "w") as fh:
+            fh.write(r.stderr)
+        objs.append(obj)
+    tmp = LIB + ".tmp"
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

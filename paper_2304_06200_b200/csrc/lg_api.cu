@@ -1,0 +1,1188 @@
+// Host orchestration and the C ABI (include/leangrape_b200.h).
+//
+// lg_problem_create  ~ ControlProblem + CostTerm validation + device upload
+//                      (src/costs.py:96-168); builds the union ELL pattern of
+//                      H_s and every h_c so that all N step generators share
+//                      one index structure.
+// lg_eval            ~ composite_grad (src/costs.py:515-546):
+//   1. lg_k_prep_*     all N step generators A_n + bit-exact planner inputs
+//   2. lg_k_plans      all N x (1 + K_c) plans on the device; guarded entries
+//                      re-planned exactly on the host (lg_planner.cuh)
+//   3. lg_k_forward    forward sweep (all trajectories, all steps)
+//   4. lg_k_trsum      running gate traces (between sweeps)
+//   5. lg_k_backward   backward sweep: adjoint, derivative products, costates
+//   6. lg_k_finalize   cost + gradient
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/leangrape_b200.h"
+#include "lg_final.cuh"
+#include "lg_numpy.cuh"
+#include "lg_planner.cuh"
+#include "lg_types.h"
+
+extern "C" void* lg_forward_kernel(int multi);
+extern "C" void* lg_backward_kernel(int multi);
+extern "C" void* lg_trsum_kernel();
+extern "C" void* lg_finalize_kernel();
+extern "C" void* lg_prep_sparse_kernel();
+extern "C" void* lg_prep_dense_kernel();
+extern "C" void* lg_plans_kernel();
+extern "C" void* lg_gather_kernel();
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(LG_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Mat {
+  bool dense = false;
+  long n = 0;
+  std::vector<long> indptr, indices;  // CSR
+  std::vector<double2> vals;          // CSR values or dense column-major
+  long nnz() const { return dense ? n * n : (long)indices.size(); }
+};
+
+int parse_mat(const lg_matrix& m, long d, Mat* out, const char* what) {
+  if (m.n != d) return fail(LG_INVALID_ARG, std::string(what) + " has mismatched shape");
+  out->dense = m.dense != 0;
+  out->n = d;
+  if (out->dense) {
+    if (!m.values) return fail(LG_INVALID_ARG, std::string(what) + ": missing dense values");
+    out->vals.resize((size_t)d * d);
+    std::memcpy(out->vals.data(), m.values, sizeof(double2) * d * d);
+  } else {
+    if (!m.row_offsets || (m.nnz && (!m.col_indices || !m.values)))
+      return fail(LG_INVALID_ARG, std::string(what) + ": missing CSR arrays");
+    out->indptr.assign(m.row_offsets, m.row_offsets + d + 1);
+    out->indices.assign(m.col_indices, m.col_indices + m.nnz);
+    out->vals.resize(m.nnz);
+    if (m.nnz) std::memcpy(out->vals.data(), m.values, sizeof(double2) * m.nnz);
+    if (out->indptr[0] != 0 || out->indptr[d] != m.nnz)
+      return fail(LG_INVALID_ARG, std::string(what) + ": malformed row offsets");
+    for (long i = 0; i < d; ++i) {
+      if (out->indptr[i + 1] < out->indptr[i]) return fail(LG_INVALID_ARG, std::string(what) + ": malformed row offsets");
+      for (long k = out->indptr[i]; k < out->indptr[i + 1]; ++k) {
+        if (out->indices[k] < 0 || out->indices[k] >= d)
+          return fail(LG_INVALID_ARG, std::string(what) + ": column index out of range");
+        if (k > out->indptr[i] && out->indices[k] <= out->indices[k - 1])
+          return fail(LG_INVALID_ARG, std::string(what) + ": columns must be strictly increasing per row");
+      }
+    }
+  }
+  return LG_OK;
+}
+
+// ELL of one operator (for the engine): W = widest row, padded with (col = row, value 0).
+void to_ell(const Mat& m, int* W_out, std::vector<int>& cols, std::vector<double2>& vals, std::vector<int>* rowlen) {
+  const long d = m.n;
+  int W = 0;
+  if (m.dense) {
+    W = (int)d;
+  } else {
+    for (long i = 0; i < d; ++i) W = std::max<int>(W, (int)(m.indptr[i + 1] - m.indptr[i]));
+  }
+  W = std::max(W, 1);
+  *W_out = W;
+  cols.assign((size_t)W * d, 0);
+  vals.assign((size_t)W * d, make_double2(0.0, 0.0));
+  if (rowlen) rowlen->assign(d, 0);
+  for (long i = 0; i < d; ++i) {
+    if (m.dense) {
+      for (long w = 0; w < d; ++w) {
+        cols[w * d + i] = (int)w;
+        vals[w * d + i] = m.vals[w * d + i];
+      }
+      if (rowlen) (*rowlen)[i] = (int)d;
+    } else {
+      long L = m.indptr[i + 1] - m.indptr[i];
+      for (long w = 0; w < W; ++w) {
+        if (w < L) {
+          cols[w * d + i] = (int)m.indices[m.indptr[i] + w];
+          vals[w * d + i] = m.vals[m.indptr[i] + w];
+        } else {
+          cols[w * d + i] = (int)i;
+        }
+      }
+      if (rowlen) (*rowlen)[i] = (int)L;
+    }
+  }
+}
+
+inline double2 gen_host(double2 h, double dt) { return make_double2(dt * h.y, -(dt * h.x)); }
+
+struct DevMem {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (p && !v.empty()) cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+struct Spec {
+  int kind;
+  double weight;
+  int set;
+  std::vector<double2> tgt;  // [K_set][d]
+  Mat pen;
+  int pen_W = 0;
+  int* d_pen_cols = nullptr;
+  double2* d_pen_vals = nullptr;
+  double2* d_tgt = nullptr;
+};
+
+}  // namespace
+
+struct lg_problem {
+  int device = 0;
+  long d = 0;
+  int Kc = 0;
+  bool dense = false, materialise = false;
+  double tau = 1e-8;
+  Mat hs;
+  std::vector<Mat> hc;
+  std::vector<Spec> specs;
+  // trajectories
+  int set_t0[2] = {0, 0}, set_T[2] = {0, 0};
+  int T_total = 0;
+  std::vector<double2> traj;
+  // union ELL
+  int W = 0;
+  std::vector<int> rowlen, cols, src_s, src_c, colptr, colent;
+  // control ELL
+  int Wc = 0;
+  std::vector<int> ccols, crowlen;
+  std::vector<double2> cvals;
+  // engine configuration
+  bool multi = false;
+  int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
+  long scratch_per_group = 0;
+  std::vector<int> grp_set, grp_t0, grp_nT;
+  int live_peak = 0;
+  long shard_b = 0, shard_e = 1L << 40;
+  // device: static
+  DevMem mem;
+  cudaStream_t stream = nullptr;
+  int *d_rowlen = nullptr, *d_cols = nullptr, *d_src_s = nullptr, *d_src_c = nullptr, *d_colptr = nullptr,
+      *d_colent = nullptr;
+  double2* d_hs = nullptr;
+  double2** d_hc_ptrs = nullptr;
+  double2* d_hs_dense = nullptr;
+  double2** d_hc_dense_ptrs = nullptr;
+  int* d_ccols = nullptr;
+  double2* d_traj = nullptr;
+  double2* d_scratch = nullptr;
+  unsigned* d_bar = nullptr;
+  double2* d_red = nullptr;
+  // per-dt control data
+  double cached_dt = NAN;
+  DevMem dtmem;
+  double2* d_Ac = nullptr;
+  double *d_ctrl_col = nullptr, *d_ctrl_row = nullptr, *d_ac_abs = nullptr, *d_ac_abs_dense = nullptr;
+  int *d_ctrl_nnz = nullptr, *d_ac_rowlen = nullptr;
+  // per-N buffers
+  long capN = 0;
+  DevMem nmem;
+  double* d_amps = nullptr;
+  double2* d_A = nullptr;
+  double *d_norm1 = nullptr, *d_aux_arg = nullptr, *d_parg = nullptr;
+  long long *d_sp = nullptr, *d_aux_sp = nullptr, *d_psp = nullptr;
+  int4* d_plan = nullptr;
+  int* d_flag = nullptr;
+  double2 *d_ip = nullptr, *d_fin = nullptr, *d_trp = nullptr, *d_trsum = nullptr, *d_psiN = nullptr;
+  double *d_run = nullptr, *d_grad = nullptr, *d_cost = nullptr;
+  int *d_spec_t0 = nullptr, *d_spec_K = nullptr;
+  long lastN = 0;
+  bool own_stream = true;
+  bool timing = false;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double phase_ms[4] = {0, 0, 0, 0};
+  long timed_evals = 0;
+
+  ~lg_problem() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    nmem.release();
+    dtmem.release();
+    mem.release();
+    if (stream && own_stream) cudaStreamDestroy(stream);
+  }
+  void mark(int i) {
+    if (timing) cudaEventRecord(ev[i], stream);
+  }
+  void collect() {
+    if (!timing) return;
+    cudaEventSynchronize(ev[4]);
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      phase_ms[i] += ms;
+    }
+    ++timed_evals;
+  }
+};
+
+namespace {
+
+// numpy-exact statistics of A_c = -i dt h_c (src/derivatives.py:148,166-184; src/sparse.py:90-121,201-222)
+int prepare_dt(lg_problem* p, double dt) {
+  if (p->cached_dt == dt) return LG_OK;
+  p->dtmem.release();
+  const long d = p->d;
+  const int Kc = p->Kc;
+  std::vector<double> ccol((size_t)Kc * d, 0.0), crow((size_t)Kc * d, 0.0), acabs, acabs_dense;
+  std::vector<int> cnnz((size_t)Kc * d, 0), acrow((size_t)Kc * d, 0);
+  std::vector<double2> Ac((size_t)Kc * p->Wc * d, make_double2(0.0, 0.0));
+  if (!p->dense && p->materialise) acabs.assign((size_t)Kc * p->Wc * d, 0.0);
+  if (p->dense && p->materialise) acabs_dense.assign((size_t)Kc * d * d, 0.0);
+  for (int c = 0; c < Kc; ++c) {
+    const Mat& m = p->hc[c];
+    for (size_t q = 0; q < (size_t)p->Wc * d; ++q) Ac[(size_t)c * p->Wc * d + q] = gen_host(p->cvals[(size_t)c * p->Wc * d + q], dt);
+    if (m.dense) {
+      std::vector<double> a((size_t)d * d);
+      for (size_t q = 0; q < a.size(); ++q) {
+        double2 g = gen_host(m.vals[q], dt);
+        a[q] = lg_np_cabs(g.x, g.y);
+      }
+      for (long j = 0; j < d; ++j) {
+        auto get = [&](long k) { return a[(size_t)j * d + k]; };
+        ccol[(size_t)c * d + j] = lg_np_pairwise(get, 0, d);
+      }
+      for (long i = 0; i < d; ++i) {
+        double r = 0.0;
+        for (long j = 0; j < d; ++j) r = r + a[(size_t)j * d + i];
+        crow[(size_t)c * d + i] = r;
+        cnnz[(size_t)c * d + i] = (int)d;
+      }
+      if (!acabs_dense.empty()) std::copy(a.begin(), a.end(), acabs_dense.begin() + (size_t)c * d * d);
+    } else {
+      std::vector<double> colsum(d, 0.0);
+      for (long i = 0; i < d; ++i) {
+        const long k0 = m.indptr[i], k1 = m.indptr[i + 1];
+        std::vector<double> av;
+        for (long k = k0; k < k1; ++k) {
+          double2 g = gen_host(m.vals[k], dt);
+          double a = lg_np_cabs(g.x, g.y);
+          av.push_back(a);
+          colsum[m.indices[k]] = colsum[m.indices[k]] + a;  // bincount: sequential, CSR order
+        }
+        auto get = [&](long k) { return av[k]; };
+        crow[(size_t)c * d + i] = lg_np_reduce(get, 0, (long)av.size());
+        cnnz[(size_t)c * d + i] = (int)av.size();
+        acrow[(size_t)c * d + i] = (int)av.size();
+        if (!acabs.empty())
+          for (size_t k = 0; k < av.size(); ++k) acabs[((size_t)c * p->Wc + k) * d + i] = av[k];
+        if (!acabs_dense.empty())
+          for (long k = k0; k < k1; ++k) acabs_dense[(size_t)c * d * d + (size_t)m.indices[k] * d + i] = av[k - k0];
+      }
+      std::copy(colsum.begin(), colsum.end(), ccol.begin() + (size_t)c * d);
+    }
+  }
+  p->d_Ac = p->dtmem.upload(Ac);
+  p->d_ctrl_col = p->dtmem.upload(ccol);
+  p->d_ctrl_row = p->dtmem.upload(crow);
+  p->d_ctrl_nnz = p->dtmem.upload(cnnz);
+  p->d_ac_rowlen = p->dtmem.upload(acrow);
+  p->d_ac_abs = acabs.empty() ? nullptr : p->dtmem.upload(acabs);
+  p->d_ac_abs_dense = acabs_dense.empty() ? nullptr : p->dtmem.upload(acabs_dense);
+  if (!p->d_Ac || !p->d_ctrl_col) return fail(LG_CUDA_ERROR, "device allocation failed (per-dt data)");
+  p->cached_dt = dt;
+  return LG_OK;
+}
+
+int ensure_N(lg_problem* p, long N) {
+  if (N <= p->capN) return LG_OK;
+  p->nmem.release();
+  const long d = p->d;
+  const int Kc = p->Kc, S = (int)p->specs.size(), T = p->T_total;
+  DevMem& m = p->nmem;
+  p->d_amps = m.alloc<double>((size_t)N * Kc);
+  p->d_A = m.alloc<double2>((size_t)N * p->W * d);
+  p->d_norm1 = m.alloc<double>(N);
+  p->d_sp = m.alloc<long long>(N);
+  p->d_aux_arg = m.alloc<double>((size_t)N * Kc);
+  p->d_aux_sp = m.alloc<long long>((size_t)N * Kc);
+  p->d_parg = m.alloc<double>((size_t)N * (Kc + 1));
+  p->d_psp = m.alloc<long long>((size_t)N * (Kc + 1));
+  p->d_plan = m.alloc<int4>((size_t)N * (Kc + 1));
+  p->d_flag = m.alloc<int>(1);
+  p->d_ip = m.alloc<double2>((size_t)N * std::max(S, 1) * Kc * std::max(T, 1));
+  p->d_fin = m.alloc<double2>((size_t)std::max(S, 1) * std::max(T, 1));
+  p->d_run = m.alloc<double>((size_t)std::max(S, 1) * std::max(T, 1));
+  p->d_trp = m.alloc<double2>((size_t)std::max(S, 1) * N * std::max(T, 1));
+  p->d_trsum = m.alloc<double2>((size_t)std::max(S, 1) * N);
+  p->d_psiN = m.alloc<double2>((size_t)std::max(T, 1) * d);
+  p->d_grad = m.alloc<double>((size_t)N * Kc);
+  p->d_cost = m.alloc<double>(1);
+  std::vector<int> st0(std::max(S, 1), 0), sK(std::max(S, 1), 0);
+  for (int s = 0; s < S; ++s) {
+    st0[s] = p->set_t0[p->specs[s].set];
+    sK[s] = p->set_T[p->specs[s].set];
+  }
+  p->d_spec_t0 = m.upload(st0);
+  p->d_spec_K = m.upload(sK);
+  if (!p->d_cost || !p->d_A || !p->d_spec_K) return fail(LG_CUDA_ERROR, "device allocation failed (per-step buffers)");
+  p->capN = N;
+  return LG_OK;
+}
+
+int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop = false) {
+  cudaError_t e = coop ? cudaLaunchCooperativeKernel(f, grid, block, args, smem, st)
+                       : cudaLaunchKernel(f, grid, block, args, smem, st);
+  if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return LG_OK;
+}
+
+// Steps 1-2: generators, planner inputs, plans (all steps at once).
+int prepare_steps(lg_problem* p, long N, double dt, bool need_aux) {
+  p->mark(0);
+  int rc = prepare_dt(p, dt);
+  if (rc) return rc;
+  LgPrepArgs P{};
+  P.d = (int)p->d;
+  P.Kc = p->Kc;
+  P.N = (int)N;
+  P.dt = dt;
+  P.amps = p->d_amps;
+  P.dense = p->dense;
+  P.materialise = p->materialise;
+  P.W = p->W;
+  P.rowlen = p->d_rowlen;
+  P.src_s = p->d_src_s;
+  P.src_c = p->d_src_c;
+  P.hs_vals = p->d_hs;
+  P.hc_vals = p->d_hc_ptrs;
+  P.colptr = p->d_colptr;
+  P.colent = p->d_colent;
+  P.hs_dense = p->d_hs_dense;
+  P.hc_dense = p->d_hc_dense_ptrs;
+  P.ctrl_col = p->d_ctrl_col;
+  P.ctrl_row = p->d_ctrl_row;
+  P.ctrl_nnz = p->d_ctrl_nnz;
+  P.Wc = p->Wc;
+  P.ac_rowlen = p->d_ac_rowlen;
+  P.ac_abs = p->d_ac_abs;
+  P.ac_abs_dense = p->d_ac_abs_dense;
+  P.A = p->d_A;
+  P.norm1 = p->d_norm1;
+  P.sp = p->d_sp;
+  P.aux_arg = p->d_aux_arg;
+  P.aux_sp = p->d_aux_sp;
+  void* args[] = {&P};
+  rc = launch(p->dense ? lg_prep_dense_kernel() : lg_prep_sparse_kernel(), dim3((unsigned)N), dim3(256), args, 0,
+              p->stream);
+  if (rc) return rc;
+  int Kc = p->Kc;
+  int count = (int)(N * (Kc + 1));
+  int Ni = (int)N;
+  void* gargs[] = {&p->d_norm1, &p->d_sp, &p->d_aux_arg, &p->d_aux_sp, &Ni, &Kc, &p->d_parg, &p->d_psp};
+  rc = launch(lg_gather_kernel(), dim3((count + 255) / 256), dim3(256), gargs, 0, p->stream);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(p->d_flag, 0, sizeof(int), p->stream));
+  double tau = p->tau, up = lg_u_prime();
+  void* pargs[] = {&p->d_parg, &p->d_psp, &count, &tau, &up, &p->d_plan, &p->d_flag};
+  rc = launch(lg_plans_kernel(), dim3((count + 127) / 128), dim3(128), pargs, 0, p->stream);
+  if (rc) return rc;
+  int flagged = 0;
+  CK(cudaMemcpyAsync(&flagged, p->d_flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (flagged) {
+    std::vector<int4> plans(count);
+    std::vector<double> arg(count);
+    std::vector<long long> sp(count);
+    CK(cudaMemcpy(plans.data(), p->d_plan, sizeof(int4) * count, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(arg.data(), p->d_parg, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sp.data(), p->d_psp, sizeof(long long) * count, cudaMemcpyDeviceToHost));
+    bool changed = false;
+    for (int q = 0; q < count; ++q) {
+      if (plans[q].z == 0) continue;
+      const bool aux = (q % (Kc + 1)) != 0;
+      if (plans[q].z & LG_PLAN_UNCERTAIN) {
+        LgPlannerCtx cx{lg_u_prime(), 0};
+        LgPlan hp = lg_make_plan(cx, arg[q], (long)sp[q], p->tau, 60, 10000);
+        plans[q] = make_int4(hp.order, hp.scaling, hp.status, 0);
+        changed = true;
+      }
+      if (plans[q].z == LG_PLAN_BADARG) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "norm1_a must be non-negative, got %g", arg[q]);
+        return fail(LG_INVALID_ARG, buf);
+      }
+      if (plans[q].z == LG_PLAN_INFEASIBLE && (need_aux || !aux)) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "no feasible (order, scaling) pair for norm1=%g, sigma_prime=%lld, tau=%g within order<=60, "
+                      "scaling<=10000",
+                      arg[q], (long long)sp[q], p->tau);
+        return fail(LG_PLANNING_INFEASIBLE, buf);
+      }
+    }
+    if (changed) CK(cudaMemcpy(p->d_plan, plans.data(), sizeof(int4) * count, cudaMemcpyHostToDevice));
+  }
+  return LG_OK;
+}
+
+LgEngineArgs engine_args(lg_problem* p, long N) {
+  LgEngineArgs E{};
+  E.d = (int)p->d;
+  E.N = (int)N;
+  E.Kc = p->Kc;
+  E.W = p->W;
+  E.Wc = p->Wc;
+  E.n_specs = (int)p->specs.size();
+  for (int s = 0; s < E.n_specs; ++s) {
+    const Spec& sp = p->specs[s];
+    E.spec[s].kind = sp.kind;
+    E.spec[s].weight = sp.weight;
+    E.spec[s].set = sp.set;
+    E.spec[s].pen_W = sp.pen_W;
+    E.spec[s].pen_cols = sp.d_pen_cols;
+    E.spec[s].pen_vals = sp.d_pen_vals;
+    E.spec[s].tgt = sp.d_tgt;
+    E.set_spec[sp.set][E.set_nspec[sp.set]++] = s;
+  }
+  for (int k = 0; k < 2; ++k) {
+    E.set_t0[k] = p->set_t0[k];
+    E.set_T[k] = p->set_T[k];
+  }
+  E.T_total = p->T_total;
+  E.n_groups = p->n_groups;
+  E.n_slabs = p->n_slabs;
+  for (int g = 0; g < p->n_groups; ++g) {
+    E.grp_set[g] = p->grp_set[g];
+    E.grp_t0[g] = p->grp_t0[g];
+    E.grp_nT[g] = p->grp_nT[g];
+  }
+  E.A_cols = p->d_cols;
+  E.A = p->d_A;
+  E.Ac_cols = p->d_ccols;
+  E.Ac = p->d_Ac;
+  E.plan = p->d_plan;
+  E.psi0 = p->d_traj;
+  E.scratch = p->d_scratch;
+  E.scratch_per_group = p->scratch_per_group;
+  E.bar = p->d_bar;
+  E.red = p->d_red;
+  E.red_cap = p->red_cap;
+  E.smem_bytes = p->smem_bytes;
+  E.smem_mode = p->smem_mode;
+  E.ip = p->d_ip;
+  E.fin = p->d_fin;
+  E.run = p->d_run;
+  E.trp = p->d_trp;
+  E.psiN = p->d_psiN;
+  E.trsum = p->d_trsum;
+  return E;
+}
+
+LgFinalArgs final_args(lg_problem* p, long N, const double2* ip, const double2* fin, const double* run,
+                       const double2* trp, double* grad, double* cost) {
+  LgFinalArgs F{};
+  F.N = (int)N;
+  F.Kc = p->Kc;
+  F.n_specs = (int)p->specs.size();
+  F.T_total = p->T_total;
+  for (int s = 0; s < F.n_specs; ++s) {
+    F.kind[s] = p->specs[s].kind;
+    F.weight[s] = p->specs[s].weight;
+    F.t0[s] = p->set_t0[p->specs[s].set];
+    F.K[s] = p->set_T[p->specs[s].set];
+  }
+  F.ip = ip;
+  F.fin = fin;
+  F.run = run;
+  F.trp = trp;
+  F.grad = grad;
+  F.cost = cost;
+  return F;
+}
+
+// Steps 3-6 with amplitudes already on the device.
+int run_sweeps(lg_problem* p, long N, bool grad) {
+  const int S = (int)p->specs.size(), T = p->T_total;
+  CK(cudaMemsetAsync(p->d_run, 0, sizeof(double) * std::max(S, 1) * std::max(T, 1), p->stream));
+  CK(cudaMemsetAsync(p->d_fin, 0, sizeof(double2) * std::max(S, 1) * std::max(T, 1), p->stream));
+  if (grad) CK(cudaMemsetAsync(p->d_ip, 0, sizeof(double2) * N * std::max(S, 1) * p->Kc * std::max(T, 1), p->stream));
+  CK(cudaMemsetAsync(p->d_trp, 0, sizeof(double2) * std::max(S, 1) * N * std::max(T, 1), p->stream));
+  CK(cudaMemsetAsync(p->d_bar, 0, sizeof(unsigned) * 4 * std::max(p->n_groups, 1), p->stream));
+  LgEngineArgs E = engine_args(p, N);
+  void* eargs[] = {&E};
+  const dim3 grid(p->n_groups * p->n_slabs), block(p->threads);
+  int rc = LG_OK;
+  p->mark(1);
+  if (p->n_groups > 0) rc = launch(lg_forward_kernel(p->multi), grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+  if (rc) return rc;
+  p->mark(2);
+  if (grad && S > 0 && p->n_groups > 0) {
+    int Ni = (int)N, Sv = S, Tv = T;
+    long cnt = (long)S * N;
+    void* targs[] = {&p->d_trp, &Sv, &Ni, &Tv, &p->d_spec_t0, &p->d_spec_K, &p->d_trsum};
+    rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
+    if (rc) return rc;
+    rc = launch(lg_backward_kernel(p->multi), grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+    if (rc) return rc;
+  }
+  p->mark(3);
+  LgFinalArgs F = final_args(p, N, p->d_ip, p->d_fin, p->d_run, p->d_trp, p->d_grad, p->d_cost);
+  void* fargs[] = {&F};
+  rc = launch(lg_finalize_kernel(), dim3((unsigned)std::min<long>((N * p->Kc + 255) / 256 + 1, 1024)), dim3(256),
+              fargs, 0, p->stream);
+  if (rc) return rc;
+  p->mark(4);
+  p->lastN = N;
+  return LG_OK;
+}
+
+int check_field(lg_problem* p, long N, double dt, const double* amps) {
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  if (N < 1) return fail(LG_INVALID_ARG, "need at least one step and one channel");
+  if (!(dt > 0.0)) return fail(LG_INVALID_ARG, "dt must be positive");
+  if (amps)
+    for (long q = 0; q < N * p->Kc; ++q)
+      if (!std::isfinite(amps[q])) return fail(LG_INVALID_ARG, "control amplitudes must be finite");
+  return LG_OK;
+}
+
+// Choose the work decomposition and the shared-memory placement.
+int configure(lg_problem* p) {
+  int dev = p->device, nsm = 0, smem_optin = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const long d = p->d;
+  const char* force = std::getenv("LG_ENGINE");
+  bool multi = d > 4096;
+  if (force && std::string(force) == "multi") multi = true;
+  if (force && std::string(force) == "single") multi = false;
+  int nsets = (p->set_T[0] > 0) + (p->set_T[1] > 0);
+  p->grp_set.clear();
+  p->grp_t0.clear();
+  p->grp_nT.clear();
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    const int K = hi - lo;
+    if (K <= 0) continue;
+    int ng = 1;
+    if (!multi && d > 256) ng = std::min(K, std::max(1, 64 / std::max(nsets, 1)));
+    for (int g = 0; g < ng; ++g) {
+      int a = (int)((long)K * g / ng), b = (int)((long)K * (g + 1) / ng);
+      p->grp_set.push_back(s);
+      p->grp_t0.push_back(p->set_t0[s] + lo + a);
+      p->grp_nT.push_back(b - a);
+    }
+  }
+  p->n_groups = (int)p->grp_set.size();
+  if (p->n_groups > 64) return fail(LG_UNSUPPORTED, "too many trajectory groups");
+  int Tmax = 1, Imax = 1;
+  for (int g = 0; g < p->n_groups; ++g) Tmax = std::max(Tmax, p->grp_nT[g]);
+  int nspec[2] = {0, 0};
+  for (auto& s : p->specs) nspec[s.set]++;
+  Imax = std::max({1, nspec[0], nspec[1]});
+  const long cstate = (long)Tmax * (1 + Imax), cxc = (long)(p->Kc + 1) * Tmax, cmax = std::max(cstate, cxc);
+  const long vecs = 2 * cstate + cxc + 2 * cmax;
+  p->scratch_per_group = vecs * d;
+  p->live_peak = (int)((vecs + Tmax - 1) / Tmax);
+  p->red_cap = (int)std::max<long>(64, (long)p->Kc * Tmax * Imax + 32);
+  p->multi = multi;
+  const long base = 2L * p->red_cap * (long)sizeof(double2);
+  const long budget = std::min<long>(smem_optin, 220 * 1024);
+  if (multi) {
+    p->threads = 1024;
+    p->n_slabs = std::max(1, nsm / std::max(1, p->n_groups));
+    p->smem_mode = 0;
+    p->smem_bytes = (int)base;
+  } else {
+    p->threads = d <= 256 ? 512 : 1024;
+    p->n_slabs = 1;
+    const long full = vecs * d * (long)sizeof(double2), an = (long)p->W * d * sizeof(double2),
+               tb = 2 * cmax * d * (long)sizeof(double2);
+    if (base + full + an <= budget) {
+      p->smem_mode = 1 | 4;
+      p->smem_bytes = (int)(base + full + an);
+    } else if (base + full <= budget) {
+      p->smem_mode = 1;
+      p->smem_bytes = (int)(base + full);
+    } else if (base + tb <= budget) {
+      p->smem_mode = 2;
+      p->smem_bytes = (int)(base + tb);
+    } else {
+      p->smem_mode = 0;
+      p->smem_bytes = (int)base;
+    }
+  }
+  for (int mm = 0; mm < 2; ++mm) {
+    CK(cudaFuncSetAttribute(lg_forward_kernel(mm), cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(lg_backward_kernel(mm), cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  }
+  if (multi) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lg_backward_kernel(1), p->threads, p->smem_bytes));
+    if (per_sm * nsm < p->n_groups * p->n_slabs)
+      return fail(LG_CUDA_ERROR, "cooperative sweep does not fit the device");
+  }
+  p->d_scratch = p->mem.alloc<double2>((size_t)p->scratch_per_group * p->n_groups);
+  p->d_bar = p->mem.alloc<unsigned>(4 * (size_t)std::max(p->n_groups, 1));
+  p->d_red = p->mem.alloc<double2>((size_t)2 * p->red_cap * p->n_slabs * std::max(p->n_groups, 1));
+  if (!p->d_scratch || !p->d_bar || !p->d_red) return fail(LG_CUDA_ERROR, "device allocation failed (scratch)");
+  return LG_OK;
+}
+
+int build_problem(const lg_problem_desc* D, lg_problem* p) {
+  if (!D) return fail(LG_INVALID_ARG, "null descriptor");
+  const long d = D->h_static.n;
+  if (d < 1) return fail(LG_INVALID_ARG, "empty Hamiltonian");
+  if (D->n_channels < 1) return fail(LG_INVALID_ARG, "need at least one control channel");
+  if (D->n_channels > LG_MAX_CHANNELS) return fail(LG_UNSUPPORTED, "more than 16 control channels");
+  if (!(D->tau > 0.0)) return fail(LG_INVALID_ARG, "tau must be positive");
+  p->d = d;
+  p->Kc = D->n_channels;
+  p->tau = D->tau;
+  p->device = D->device;
+  int rc = parse_mat(D->h_static, d, &p->hs, "static Hamiltonian");
+  if (rc) return rc;
+  p->hc.resize(p->Kc);
+  for (int c = 0; c < p->Kc; ++c) {
+    rc = parse_mat(D->h_controls[c], d, &p->hc[c], "control operator");
+    if (rc) return rc;
+  }
+  p->dense = p->hs.dense;
+  for (auto& m : p->hc) p->dense = p->dense || m.dense;
+  p->materialise = 2 * d <= 256;  // src/derivatives.py:29,199-202
+  if (p->dense && d > 512) return fail(LG_UNSUPPORTED, "dense operators with d > 512 use the DMMA path (not in this build)");
+  // ---- terms and trajectory sets
+  if (D->n_terms > LG_MAX_SPECS) return fail(LG_UNSUPPORTED, "more than 8 cost terms");
+  bool has_state = false, has_gate = false;
+  for (int t = 0; t < D->n_terms; ++t) {
+    const lg_cost_term& ct = D->terms[t];
+    if (ct.kind < 0 || ct.kind > 4) return fail(LG_INVALID_ARG, "unknown cost kind");
+    if (ct.weight < 0.0) return fail(LG_INVALID_ARG, "cost weights must be non-negative");
+    (ct.kind <= LG_STATE_RUNNING_INFIDELITY ? has_state : has_gate) = true;
+  }
+  const long Ks = D->n_states, Kg = D->n_basis;
+  if ((has_state || D->n_terms == 0) && (Ks < 1 || !D->initial_states))
+    return fail(LG_INVALID_ARG, "state-transfer terms require problem.initial_state");
+  std::vector<double2> basis_v;
+  long Kgate = 0;
+  if (has_gate) {
+    if (Kg > 0 && D->basis) {
+      Kgate = Kg;
+      basis_v.resize((size_t)Kg * d);
+      std::memcpy(basis_v.data(), D->basis, sizeof(double2) * Kg * d);
+    } else {
+      Kgate = d;  // computational basis (src/costs.py:393-397)
+      basis_v.assign((size_t)d * d, make_double2(0.0, 0.0));
+      for (long h = 0; h < d; ++h) basis_v[(size_t)h * d + h] = make_double2(1.0, 0.0);
+    }
+  }
+  std::vector<double2> states_v;
+  if (Ks > 0 && D->initial_states && (has_state || D->n_terms == 0)) {
+    states_v.resize((size_t)Ks * d);
+    std::memcpy(states_v.data(), D->initial_states, sizeof(double2) * Ks * d);
+  }
+  // merge identical sets (same trajectories drive both kinds of term)
+  bool merged = has_gate && !states_v.empty() && states_v.size() == basis_v.size() &&
+                std::memcmp(states_v.data(), basis_v.data(), sizeof(double2) * states_v.size()) == 0;
+  p->traj.clear();
+  if (!states_v.empty()) {
+    p->set_t0[0] = 0;
+    p->set_T[0] = (int)Ks;
+    p->traj.insert(p->traj.end(), states_v.begin(), states_v.end());
+  }
+  if (has_gate) {
+    if (merged) {
+      p->set_t0[1] = 0;
+      p->set_T[1] = 0;  // gate terms ride on set 0's trajectories
+    } else {
+      p->set_t0[1] = (int)(p->traj.size() / d);
+      p->set_T[1] = (int)Kgate;
+      p->traj.insert(p->traj.end(), basis_v.begin(), basis_v.end());
+    }
+  }
+  p->T_total = (int)(p->traj.size() / d);
+  // sharding (multi-GPU): each set propagates only trajectories [shard_begin, shard_end) of itself
+  p->shard_b = D->shard_end > 0 ? D->shard_begin : 0;
+  p->shard_e = D->shard_end > 0 ? D->shard_end : (1L << 40);
+  for (int t = 0; t < D->n_terms; ++t) {
+    const lg_cost_term& ct = D->terms[t];
+    Spec sp;
+    sp.kind = ct.kind;
+    sp.weight = ct.weight;
+    sp.set = (ct.kind <= LG_STATE_RUNNING_INFIDELITY || merged) ? 0 : 1;
+    if (sp.kind == LG_GATE_RUNNING_INFIDELITY && D->shard_end > 0)
+      return fail(LG_UNSUPPORTED, "sharded running gate cost needs the split forward/backward API");
+    const int K = p->set_T[sp.set];
+    if (ct.kind == LG_STATE_PENALTY) {
+      rc = parse_mat(ct.penalty, d, &sp.pen, "penalty operator");
+      if (rc) return rc;
+    } else {
+      if (!ct.targets) return fail(LG_INVALID_ARG, "cost term requires target states / images");
+      sp.tgt.resize((size_t)K * d);
+      std::memcpy(sp.tgt.data(), ct.targets, sizeof(double2) * K * d);
+    }
+    p->specs.push_back(std::move(sp));
+  }
+  // ---- union ELL pattern (sparse) or full pattern (dense)
+  if (p->dense) {
+    p->W = (int)d;
+    p->rowlen.assign(d, (int)d);
+    p->cols.resize((size_t)d * d);
+    for (long w = 0; w < d; ++w)
+      for (long i = 0; i < d; ++i) p->cols[w * d + i] = (int)w;
+  } else {
+    std::vector<std::vector<int>> rows(d);
+    for (long i = 0; i < d; ++i) {
+      std::vector<int>& r = rows[i];
+      for (long k = p->hs.indptr[i]; k < p->hs.indptr[i + 1]; ++k) r.push_back((int)p->hs.indices[k]);
+      for (auto& m : p->hc)
+        for (long k = m.indptr[i]; k < m.indptr[i + 1]; ++k) r.push_back((int)m.indices[k]);
+      std::sort(r.begin(), r.end());
+      r.erase(std::unique(r.begin(), r.end()), r.end());
+      p->W = std::max<int>(p->W, (int)r.size());
+    }
+    p->W = std::max(p->W, 1);
+    if (p->W > LG_MAXW) return fail(LG_UNSUPPORTED, "more than 64 stored elements per row");
+    const int W = p->W;
+    p->rowlen.assign(d, 0);
+    p->cols.assign((size_t)W * d, 0);
+    p->src_s.assign((size_t)W * d, -1);
+    p->src_c.assign((size_t)p->Kc * W * d, -1);
+    for (long i = 0; i < d; ++i) {
+      const auto& r = rows[i];
+      p->rowlen[i] = (int)r.size();
+      for (int w = 0; w < W; ++w) p->cols[(size_t)w * d + i] = w < (int)r.size() ? r[w] : (int)i;
+      auto fill = [&](const Mat& m, int* dst) {
+        size_t w = 0;
+        for (long k = m.indptr[i]; k < m.indptr[i + 1]; ++k) {
+          while (r[w] != m.indices[k]) ++w;
+          dst[w * d + i] = (int)k;
+        }
+      };
+      fill(p->hs, p->src_s.data());
+      for (int c = 0; c < p->Kc; ++c) fill(p->hc[c], p->src_c.data() + (size_t)c * W * d);
+    }
+    // transposed slot lists: for each column, slots in ascending row order
+    p->colptr.assign(d + 1, 0);
+    for (long i = 0; i < d; ++i)
+      for (int w = 0; w < p->rowlen[i]; ++w) p->colptr[p->cols[(size_t)w * d + i] + 1]++;
+    for (long j = 0; j < d; ++j) p->colptr[j + 1] += p->colptr[j];
+    p->colent.assign(p->colptr[d], 0);
+    std::vector<int> fillp(p->colptr.begin(), p->colptr.end() - 1);
+    for (long i = 0; i < d; ++i)
+      for (int w = 0; w < p->rowlen[i]; ++w) p->colent[fillp[p->cols[(size_t)w * d + i]]++] = (int)(w * d + i);
+  }
+  // ---- control ELL (engine) — raw h_c values; A_c is formed per dt
+  {
+    int Wc = 1;
+    for (auto& m : p->hc) {
+      if (m.dense) Wc = std::max<int>(Wc, (int)d);
+      else
+        for (long i = 0; i < d; ++i) Wc = std::max<int>(Wc, (int)(m.indptr[i + 1] - m.indptr[i]));
+    }
+    if (!p->dense && Wc > LG_MAXW) return fail(LG_UNSUPPORTED, "more than 64 stored elements per control row");
+    p->Wc = Wc;
+    p->ccols.assign((size_t)p->Kc * Wc * d, 0);
+    p->cvals.assign((size_t)p->Kc * Wc * d, make_double2(0.0, 0.0));
+    for (int c = 0; c < p->Kc; ++c) {
+      const Mat& m = p->hc[c];
+      for (long i = 0; i < d; ++i) {
+        for (int w = 0; w < Wc; ++w) {
+          size_t q = ((size_t)c * Wc + w) * d + i;
+          if (m.dense) {
+            p->ccols[q] = w;
+            p->cvals[q] = m.vals[(size_t)w * d + i];
+          } else {
+            long L = m.indptr[i + 1] - m.indptr[i];
+            if (w < L) {
+              p->ccols[q] = (int)m.indices[m.indptr[i] + w];
+              p->cvals[q] = m.vals[m.indptr[i] + w];
+            } else {
+              p->ccols[q] = (int)i;
+            }
+          }
+        }
+      }
+    }
+  }
+  // ---- device upload
+  CK(cudaSetDevice(p->device));
+  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  DevMem& M = p->mem;
+  p->d_rowlen = M.upload(p->rowlen);
+  p->d_cols = M.upload(p->cols);
+  p->d_ccols = M.upload(p->ccols);
+  p->d_traj = M.upload(p->traj);
+  if (p->dense) {
+    std::vector<double2> hsd = p->hs.dense ? p->hs.vals : std::vector<double2>((size_t)d * d, make_double2(0, 0));
+    if (!p->hs.dense)
+      for (long i = 0; i < d; ++i)
+        for (long k = p->hs.indptr[i]; k < p->hs.indptr[i + 1]; ++k) hsd[(size_t)p->hs.indices[k] * d + i] = p->hs.vals[k];
+    p->d_hs_dense = M.upload(hsd);
+    std::vector<double2*> ptrs(p->Kc);
+    for (int c = 0; c < p->Kc; ++c) {
+      const Mat& m = p->hc[c];
+      std::vector<double2> v = m.dense ? m.vals : std::vector<double2>((size_t)d * d, make_double2(0, 0));
+      if (!m.dense)
+        for (long i = 0; i < d; ++i)
+          for (long k = m.indptr[i]; k < m.indptr[i + 1]; ++k) v[(size_t)m.indices[k] * d + i] = m.vals[k];
+      ptrs[c] = M.upload(v);
+    }
+    p->d_hc_dense_ptrs = M.upload(ptrs);
+  } else {
+    p->d_src_s = M.upload(p->src_s);
+    p->d_src_c = M.upload(p->src_c);
+    p->d_colptr = M.upload(p->colptr);
+    p->d_colent = M.upload(p->colent);
+    p->d_hs = M.upload(p->hs.vals);
+    std::vector<double2*> ptrs(p->Kc);
+    for (int c = 0; c < p->Kc; ++c) ptrs[c] = M.upload(p->hc[c].vals);
+    p->d_hc_ptrs = M.upload(ptrs);
+  }
+  for (auto& sp : p->specs) {
+    if (sp.kind == LG_STATE_PENALTY) {
+      std::vector<int> pc;
+      std::vector<double2> pv;
+      to_ell(sp.pen, &sp.pen_W, pc, pv, nullptr);
+      sp.d_pen_cols = M.upload(pc);
+      sp.d_pen_vals = M.upload(pv);
+    } else {
+      sp.d_tgt = M.upload(sp.tgt);
+    }
+  }
+  if (!p->d_traj || !p->d_cols) return fail(LG_CUDA_ERROR, "device allocation failed (problem data)");
+  return configure(p);
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+const char* lg_last_error(void) { return g_err.c_str(); }
+const char* lg_version(void) { return "paper_2304_06200_b200 0.1 (sm_100a)"; }
+
+int lg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int lg_make_plan(double norm1, int64_t sigma_prime, double tau, int32_t m_max, int32_t s_max, int32_t* order,
+                 int32_t* scaling, double* bound) {
+  LgPlannerCtx cx{lg_u_prime(), 0};
+  LgPlan p = lg_make_plan(cx, norm1, (long)sigma_prime, tau, m_max, s_max);
+  if (p.status == LG_PLAN_BADARG) {
+    if (!(norm1 >= 0.0)) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "norm1_a must be non-negative, got %g", norm1);
+      return fail(LG_INVALID_ARG, buf);
+    }
+    return fail(LG_INVALID_ARG, sigma_prime < 0 ? "sigma_prime must be non-negative" : "tau must be positive");
+  }
+  if (p.status == LG_PLAN_INFEASIBLE) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "no feasible (order, scaling) pair for norm1=%g, sigma_prime=%lld, tau=%g within order<=%d, "
+                  "scaling<=%d",
+                  norm1, (long long)sigma_prime, tau, m_max, s_max);
+    return fail(LG_PLANNING_INFEASIBLE, buf);
+  }
+  *order = p.order;
+  *scaling = p.scaling;
+  *bound = p.bound;
+  return LG_OK;
+}
+
+int lg_make_plans_device(int64_t count, const double* norm1, const int64_t* sigma, double tau, int32_t* order,
+                         int32_t* scaling, int32_t* status, int32_t* n_uncertain) {
+  DevMem m;
+  double* a = m.alloc<double>(count);
+  long long* s = m.alloc<long long>(count);
+  int4* pl = m.alloc<int4>(count);
+  int* fl = m.alloc<int>(1);
+  if (!a || !s || !pl || !fl) {
+    m.release();
+    return fail(LG_CUDA_ERROR, "device allocation failed");
+  }
+  cudaMemcpy(a, norm1, sizeof(double) * count, cudaMemcpyHostToDevice);
+  cudaMemcpy(s, sigma, sizeof(long long) * count, cudaMemcpyHostToDevice);
+  cudaMemset(fl, 0, sizeof(int));
+  int cnt = (int)count;
+  double up = lg_u_prime();
+  void* args[] = {&a, &s, &cnt, &tau, &up, &pl, &fl};
+  int rc = launch(lg_plans_kernel(), dim3((cnt + 127) / 128), dim3(128), args, 0, 0);
+  std::vector<int4> h(count);
+  if (!rc) {
+    cudaError_t e = cudaMemcpy(h.data(), pl, sizeof(int4) * count, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(LG_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  m.release();
+  if (rc) return rc;
+  int unc = 0;
+  for (long q = 0; q < count; ++q) {
+    if (h[q].z & LG_PLAN_UNCERTAIN) {
+      ++unc;
+      LgPlannerCtx cx{lg_u_prime(), 0};
+      LgPlan hp = lg_make_plan(cx, norm1[q], (long)sigma[q], tau, 60, 10000);
+      h[q] = make_int4(hp.order, hp.scaling, hp.status, 0);
+    }
+    order[q] = h[q].x;
+    scaling[q] = h[q].y;
+    status[q] = h[q].z;
+  }
+  *n_uncertain = unc;
+  return LG_OK;
+}
+
+int lg_problem_create(const lg_problem_desc* desc, lg_problem** out) {
+  if (!out) return fail(LG_INVALID_ARG, "null output pointer");
+  *out = nullptr;
+  int ndev = lg_device_count();
+  if (ndev <= 0) return fail(LG_CUDA_ERROR, "no CUDA device available (this library has no CPU fallback)");
+  lg_problem* p = new lg_problem();
+  int rc = build_problem(desc, p);
+  if (rc) {
+    std::string keep = g_err;
+    delete p;
+    g_err = keep;
+    return rc;
+  }
+  *out = p;
+  return LG_OK;
+}
+
+void lg_problem_destroy(lg_problem* p) { delete p; }
+
+int lg_set_stream(lg_problem* p, void* stream) {
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  CK(cudaStreamSynchronize(p->stream));
+  if (p->own_stream && p->stream) CK(cudaStreamDestroy(p->stream));
+  p->stream = (cudaStream_t)stream;
+  p->own_stream = false;
+  return LG_OK;
+}
+
+int lg_set_timing(lg_problem* p, int enable) {
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  if (enable && !p->ev[0])
+    for (auto& e : p->ev) CK(cudaEventCreate(&e));
+  p->timing = enable != 0;
+  for (double& v : p->phase_ms) v = 0.0;
+  p->timed_evals = 0;
+  return LG_OK;
+}
+
+int lg_get_timing(lg_problem* p, double* phase_ms, int64_t* evals) {
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  for (int i = 0; i < 4; ++i) phase_ms[i] = p->phase_ms[i];
+  *evals = p->timed_evals;
+  return LG_OK;
+}
+
+int lg_eval_device(lg_problem* p, int64_t n_steps, double dt, const double* d_amps, double* d_cost, double* d_grad) {
+  int rc = check_field(p, n_steps, dt, nullptr);
+  if (rc) return rc;
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  if (d_amps != p->d_amps)
+    CK(cudaMemcpyAsync(p->d_amps, d_amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyDeviceToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, true);
+  if (rc) return rc;
+  rc = run_sweeps(p, n_steps, true);
+  if (rc) return rc;
+  if (d_cost) CK(cudaMemcpyAsync(d_cost, p->d_cost, sizeof(double), cudaMemcpyDeviceToDevice, p->stream));
+  if (d_grad)
+    CK(cudaMemcpyAsync(d_grad, p->d_grad, sizeof(double) * n_steps * p->Kc, cudaMemcpyDeviceToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  p->collect();
+  return LG_OK;
+}
+
+int lg_eval(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost, double* grad,
+            int64_t* live_vector_peak) {
+  int rc = check_field(p, n_steps, dt, amps);
+  if (rc) return rc;
+  if (p->specs.empty()) return fail(LG_INVALID_ARG, "composite cost needs at least one term");
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, true);
+  if (rc) return rc;
+  rc = run_sweeps(p, n_steps, true);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(cost, p->d_cost, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaMemcpyAsync(grad, p->d_grad, sizeof(double) * n_steps * p->Kc, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  p->collect();
+  if (live_vector_peak) *live_vector_peak = p->live_peak;
+  return LG_OK;
+}
+
+int lg_cost(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost) {
+  int rc = check_field(p, n_steps, dt, amps);
+  if (rc) return rc;
+  if (p->specs.empty()) return fail(LG_INVALID_ARG, "composite cost needs at least one term");
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, false);
+  if (rc) return rc;
+  rc = run_sweeps(p, n_steps, false);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(cost, p->d_cost, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return LG_OK;
+}
+
+int lg_forward_states(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* out) {
+  int rc = check_field(p, n_steps, dt, amps);
+  if (rc) return rc;
+  if (p->set_T[0] == 0) return fail(LG_INVALID_ARG, "problem has no initial states");
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, false);
+  if (rc) return rc;
+  rc = run_sweeps(p, n_steps, false);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, p->d_psiN + (size_t)p->set_t0[0] * p->d, sizeof(double2) * p->set_T[0] * p->d,
+                     cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return LG_OK;
+}
+
+int lg_plan_table(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* norm1, int64_t* sigma,
+                  int32_t* order, int32_t* scaling, double* aux_arg, int64_t* aux_sigma, int32_t* aux_order,
+                  int32_t* aux_scaling) {
+  int rc = check_field(p, n_steps, dt, amps);
+  if (rc) return rc;
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, true);
+  if (rc) return rc;
+  const long N = n_steps, Kc = p->Kc;
+  std::vector<int4> pl((size_t)N * (Kc + 1));
+  std::vector<long long> sp(N), asp((size_t)N * Kc);
+  CK(cudaMemcpy(norm1, p->d_norm1, sizeof(double) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(sp.data(), p->d_sp, sizeof(long long) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(aux_arg, p->d_aux_arg, sizeof(double) * N * Kc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(asp.data(), p->d_aux_sp, sizeof(long long) * N * Kc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(pl.data(), p->d_plan, sizeof(int4) * pl.size(), cudaMemcpyDeviceToHost));
+  for (long n = 0; n < N; ++n) {
+    sigma[n] = sp[n];
+    order[n] = pl[n * (Kc + 1)].x;
+    scaling[n] = pl[n * (Kc + 1)].y;
+    for (long c = 0; c < Kc; ++c) {
+      aux_sigma[n * Kc + c] = asp[n * Kc + c];
+      aux_order[n * Kc + c] = pl[n * (Kc + 1) + 1 + c].x;
+      aux_scaling[n * Kc + c] = pl[n * (Kc + 1) + 1 + c].y;
+    }
+  }
+  return LG_OK;
+}
+
+int64_t lg_raw_size(lg_problem* p, int64_t N) {
+  const long S = (long)p->specs.size(), T = p->T_total, Kc = p->Kc;
+  // ip, fin, trp (complex) + run (real)
+  return 2 * (N * S * Kc * T + S * T + S * N * T) + S * T;
+}
+
+int lg_raw_get(lg_problem* p, double* raw) {
+  const long N = p->lastN, S = (long)p->specs.size(), T = p->T_total, Kc = p->Kc;
+  double* q = raw;
+  CK(cudaMemcpy(q, p->d_ip, sizeof(double2) * N * S * Kc * T, cudaMemcpyDeviceToHost));
+  q += 2 * N * S * Kc * T;
+  CK(cudaMemcpy(q, p->d_fin, sizeof(double2) * S * T, cudaMemcpyDeviceToHost));
+  q += 2 * S * T;
+  CK(cudaMemcpy(q, p->d_trp, sizeof(double2) * S * N * T, cudaMemcpyDeviceToHost));
+  q += 2 * S * N * T;
+  CK(cudaMemcpy(q, p->d_run, sizeof(double) * S * T, cudaMemcpyDeviceToHost));
+  return LG_OK;
+}
+
+int lg_finalize_raw(int32_t n_terms, const int32_t* kinds, const double* weights, const int32_t* t0, const int32_t* K,
+                    int64_t N, int32_t Kc, int32_t T, const double* raw, double* cost, double* grad) {
+  if (n_terms < 0 || n_terms > LG_MAX_SPECS || N < 1 || Kc < 1 || T < 0) return fail(LG_INVALID_ARG, "bad sizes");
+  const long S = n_terms;
+  LgFinalArgs F{};
+  F.N = (int)N;
+  F.Kc = Kc;
+  F.n_specs = n_terms;
+  F.T_total = T;
+  for (int s = 0; s < n_terms; ++s) {
+    F.kind[s] = kinds[s];
+    F.weight[s] = weights[s];
+    F.t0[s] = t0[s];
+    F.K[s] = K[s];
+  }
+  F.ip = (const double2*)raw;
+  F.fin = F.ip + N * S * Kc * T;
+  F.trp = F.fin + S * T;
+  F.run = (const double*)(F.trp + S * N * T);
+  for (long q = 0; q < N * Kc; ++q) grad[q] = lg_final_grad(F, q);
+  *cost = lg_final_cost(F);
+  return LG_OK;
+}
+
+void lg_np_cabs_host(int64_t n, const double* z, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = lg_np_cabs(z[2 * i], z[2 * i + 1]);
+}
+double lg_np_pairwise_host(int64_t n, const double* a) {
+  auto get = [&](long k) { return a[k]; };
+  return lg_np_pairwise(get, 0, (long)n);
+}
+double lg_np_reduce_host(int64_t n, const double* a) {
+  auto get = [&](long k) { return a[k]; };
+  return lg_np_reduce(get, 0, (long)n);
+}
+
+int lg_finalize_host(lg_problem* p, int64_t N, const double* raw, double* cost, double* grad) {
+  const long S = (long)p->specs.size(), T = p->T_total, Kc = p->Kc;
+  const double2* ip = (const double2*)raw;
+  const double2* fin = ip + N * S * Kc * T;
+  const double2* trp = fin + S * T;
+  const double* run = (const double*)(trp + S * N * T);
+  LgFinalArgs F = final_args(p, N, ip, fin, run, trp, grad, cost);
+  for (long q = 0; q < N * Kc; ++q) grad[q] = lg_final_grad(F, q);
+  *cost = lg_final_cost(F);
+  return LG_OK;
+}
+
+}  // extern "C"

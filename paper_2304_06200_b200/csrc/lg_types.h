@@ -1,0 +1,106 @@
+// Device-side data descriptors shared by the host orchestration (lg_api.cu),
+// the step-preparation kernels (lg_prep.cu) and the sweep engine (lg_engine.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define LG_MAX_CHANNELS 16
+#define LG_MAX_SPECS 8
+#define LG_MAXW 64  // widest ELL row handled by the bit-exact row-sum path
+
+// Cost kinds (src/costs.py:49-61)
+enum LgKind { LGK_STATE_INF = 0, LGK_STATE_PEN = 1, LGK_STATE_RUN = 2, LGK_GATE = 3, LGK_GATE_RUN = 4 };
+
+// ---------------------------------------------------------------- step preparation (G1)
+struct LgPrepArgs {
+  int d, Kc, N;
+  double dt;
+  const double* amps;  // [N][Kc]
+  int dense;           // storage of H_n (any input dense -> dense, src/sparse.py:322-334)
+  int materialise;     // 2d <= 256 (src/derivatives.py:29,199-202)
+  // sparse: union ELL pattern of H_s and all h_c (CSR column order per row)
+  int W;
+  const int* rowlen;   // [d]
+  const int* src_s;    // [W][d] index into hs_vals or -1
+  const int* src_c;    // [Kc][W][d] index into hc_vals[c] or -1
+  const double2* hs_vals;
+  const double2* const* hc_vals;  // device array of Kc pointers
+  const int* colptr;   // [d+1] union pattern transposed (slots w*d+i sorted by row)
+  const int* colent;   // [nnz_union]
+  // dense inputs (column-major)
+  const double2* hs_dense;              // [d*d]
+  const double2* const* hc_dense;       // Kc pointers [d*d]
+  // control-generator statistics for A_c = -i dt h_c (host-computed, numpy rules)
+  const double* ctrl_col;   // [Kc][d] column abs sums
+  const double* ctrl_row;   // [Kc][d] row abs sums
+  const int* ctrl_nnz;      // [Kc][d] stored entries per row
+  int Wc;                   // sparse materialised aux needs A_c row entries in column order
+  const int* ac_rowlen;     // [Kc][d]
+  const double* ac_abs;     // [Kc][Wc][d] |A_c| entries in column order (slot w of row i)
+  const double* ac_abs_dense;  // dense materialised: [Kc][d*d] |A_c| column-major
+  // outputs
+  double2* A;               // [N][W][d] step generators (nullptr: do not store)
+  double* norm1;            // [N]
+  long long* sp;            // [N]
+  double* aux_arg;          // [N][Kc] sqrt(||aux||_1 ||aux||_inf)
+  long long* aux_sp;        // [N][Kc]
+};
+
+// ---------------------------------------------------------------- sweep engine
+struct LgSpecDev {
+  int kind;
+  double weight;
+  int set;                 // 0 = state trajectories, 1 = gate basis
+  int pen_W;               // STATE_PEN: ELL width of the penalty operator
+  const int* pen_cols;     // [W][d]
+  const double2* pen_vals; // [W][d]
+  const double2* tgt;      // [T_set][d] targets (state) / images U_T psi_h (gate), rows = set order
+};
+
+struct LgEngineArgs {
+  int d, N, Kc, W, Wc;
+  int n_specs;
+  LgSpecDev spec[LG_MAX_SPECS];
+  int set_nspec[2];
+  int set_spec[2][LG_MAX_SPECS];
+  int set_t0[2], set_T[2];   // global trajectory index range of each set
+  int T_total;
+  // groups: blockIdx.x / n_slabs = group; each group = trajectory range in one set
+  int n_groups, n_slabs, grp_T;   // trajectories per group (last may be short)
+  int grp_set[64], grp_t0[64], grp_nT[64];
+  // operators
+  const int* A_cols;        // [W][d]
+  const double2* A;         // [N][W][d]
+  const int* Ac_cols;       // [Kc][Wc][d]
+  const double2* Ac;        // [Kc][Wc][d]
+  const int4* plan;         // [N][1+Kc] (order, scaling, status, -)
+  const double2* psi0;      // [T_total][d] initial trajectories
+  // scratch
+  double2* scratch;         // per group: scratch_per_group d-vectors
+  long long scratch_per_group;  // in double2 units
+  unsigned* bar;            // per group [4]
+  double2* red;             // per group [2][red_cap][n_slabs]
+  int red_cap;
+  int smem_bytes;           // dynamic shared memory provided
+  int smem_mode;            // bit0: all state buffers in smem; bit1: term buffers in smem; bit2: A_n in smem
+  // raw outputs (indexed by global trajectory)
+  double2* ip;              // [N][n_specs][Kc][T_total]
+  double2* fin;             // [n_specs][T_total]
+  double* run;              // [n_specs][T_total]
+  double2* trp;             // [n_specs][N][T_total]
+  double2* psiN;            // [T_total][d] final states (forward -> backward)
+  const double2* trsum;     // [n_specs][N] trace sums (GATE_RUN), filled between sweeps
+};
+
+struct LgFinalArgs {
+  int N, Kc, n_specs, T_total;
+  int kind[LG_MAX_SPECS];
+  double weight[LG_MAX_SPECS];
+  int t0[LG_MAX_SPECS], K[LG_MAX_SPECS];
+  const double2* ip;
+  const double2* fin;
+  const double* run;
+  const double2* trp;
+  double* grad;   // [N][Kc]
+  double* cost;   // [1]
+};

@@ -1,0 +1,210 @@
+"""Host-side operator containers (mirror of the reference's src/sparse.py API).
+
+These are plain data holders used to *describe* a problem to the device
+library: the layouts are exactly the reference's (CSR with int64 offsets and
+indices, complex128 values, exact zeros dropped and duplicates summed at
+construction, src/sparse.py:237-270; column-major dense, :152-170).  Every
+numerical operation of an evaluation happens on the GPU; the helpers here
+(construction, linear_combine, kron, Hermiticity checks) only build and
+validate inputs, as ControlProblem does in the reference.
+
+Objects that merely expose the reference's field names (``row_offsets``,
+``col_indices``, ``values`` / ``array``) -- e.g. the reference's own
+CsrMatrix -- are accepted everywhere too.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "SparseMatrixError",
+    "CsrMatrix",
+    "DenseMatrix",
+    "build_csr_arrays",
+    "build_csr",
+    "from_dense",
+    "identity_csr",
+    "linear_combine",
+    "kron_csr",
+    "is_hermitian",
+    "to_dense",
+]
+
+
+class SparseMatrixError(ValueError):
+    """Malformed construction input or shape mismatch (src/sparse.py:37-38)."""
+
+
+@dataclass(frozen=True, eq=False)
+class CsrMatrix:
+    n_rows: int
+    n_cols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    def triplets(self):
+        rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_offsets))
+        return rows, self.col_indices.copy(), self.values.copy()
+
+    def conj_transpose(self) -> "CsrMatrix":
+        r, c, v = self.triplets()
+        return build_csr_arrays(c, r, np.conj(v), self.n_cols, self.n_rows)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.n_rows, self.n_cols), np.complex128, order="F")
+        r, c, v = self.triplets()
+        out[r, c] = v
+        return out
+
+
+@dataclass(frozen=True, eq=False)
+class DenseMatrix:
+    array: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        arr = np.asfortranarray(np.asarray(self.array, dtype=np.complex128))
+        if arr.ndim != 2:
+            raise SparseMatrixError("DenseMatrix expects a 2-d array")
+        if not np.isfinite(arr).all():
+            raise SparseMatrixError("matrix entries must be finite")
+        object.__setattr__(self, "array", arr)
+
+    @property
+    def n_rows(self):
+        return self.array.shape[0]
+
+    @property
+    def n_cols(self):
+        return self.array.shape[1]
+
+    @property
+    def shape(self):
+        return self.array.shape
+
+    @property
+    def nnz(self):
+        return self.array.size
+
+    def to_dense(self) -> np.ndarray:
+        return self.array.copy(order="F")
+
+    def conj_transpose(self) -> "DenseMatrix":
+        return DenseMatrix(self.array.conj().T)
+
+
+def build_csr_arrays(rows, cols, vals, n_rows: int, n_cols: int) -> CsrMatrix:
+    """COO -> CSR, duplicates summed in input order, exact zeros dropped."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.complex128)
+    if not (rows.shape == cols.shape == vals.shape):
+        raise SparseMatrixError("rows, cols and values must have equal length")
+    if rows.size:
+        if rows.min() < 0 or rows.max() >= n_rows or cols.min() < 0 or cols.max() >= n_cols:
+            raise SparseMatrixError("index out of range")
+        if not np.isfinite(vals).all():
+            raise SparseMatrixError("matrix entries must be finite")
+    keys = rows * np.int64(n_cols) + cols
+    uniq, inv = np.unique(keys, return_inverse=True)
+    summed = np.zeros(uniq.size, np.complex128)
+    np.add.at(summed, inv, vals)
+    keep = summed != 0
+    uniq, summed = uniq[keep], summed[keep]
+    offsets = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(np.bincount(uniq // n_cols, minlength=n_rows), out=offsets[1:])
+    return CsrMatrix(n_rows, n_cols, offsets, (uniq % n_cols).astype(np.int64), summed)
+
+
+def build_csr(triplets, n_rows: int, n_cols: int) -> CsrMatrix:
+    entries = list(triplets)
+    if not entries:
+        return build_csr_arrays(np.empty(0), np.empty(0), np.empty(0), n_rows, n_cols)
+    r, c, v = zip(*entries)
+    return build_csr_arrays(r, c, v, n_rows, n_cols)
+
+
+def from_dense(array) -> CsrMatrix:
+    a = np.asarray(array, np.complex128)
+    r, c = np.nonzero(a)
+    return build_csr_arrays(r, c, a[r, c], a.shape[0], a.shape[1])
+
+
+def identity_csr(n: int) -> CsrMatrix:
+    i = np.arange(n, dtype=np.int64)
+    return build_csr_arrays(i, i, np.ones(n, np.complex128), n, n)
+
+
+def to_dense(m) -> np.ndarray:
+    if hasattr(m, "array"):
+        return np.asarray(m.array)
+    return m.to_dense()
+
+
+def linear_combine(coeffs, mats):
+    """sum_i coeffs[i] mats[i] with the reference's operand order (src/sparse.py:313-349)."""
+    mats = list(mats)
+    coeffs = [complex(c) for c in coeffs]
+    if len(coeffs) != len(mats) or not mats:
+        raise SparseMatrixError("need one coefficient per matrix")
+    shape = mats[0].shape
+    if any(m.shape != shape for m in mats):
+        raise SparseMatrixError("shape mismatch in linear_combine")
+    if any(isinstance(m, DenseMatrix) for m in mats):
+        total = np.zeros(shape, np.complex128, order="F")
+        for c, m in zip(coeffs, mats):
+            if c != 0:
+                total += to_dense(m) * c
+        return DenseMatrix(total)
+    rs, cs, vs = [], [], []
+    for c, m in zip(coeffs, mats):
+        if c == 0 or m.nnz == 0:
+            continue
+        r, k, v = m.triplets()
+        rs.append(r)
+        cs.append(k)
+        vs.append(c * v)
+    if not rs:
+        return build_csr([], *shape)
+    return build_csr_arrays(np.concatenate(rs), np.concatenate(cs), np.concatenate(vs), *shape)
+
+
+def kron_csr(a: CsrMatrix, b: CsrMatrix) -> CsrMatrix:
+    ra, ca, va = a.triplets()
+    rb, cb, vb = b.triplets()
+    rows = (ra[:, None] * b.n_rows + rb[None, :]).ravel()
+    cols = (ca[:, None] * b.n_cols + cb[None, :]).ravel()
+    vals = (va[:, None] * vb[None, :]).ravel()
+    return build_csr_arrays(rows, cols, vals, a.n_rows * b.n_rows, a.n_cols * b.n_cols)
+
+
+def is_hermitian(m, tol: float) -> bool:
+    """max |M - M^dagger| <= tol (src/sparse.py:393-397)."""
+    if m.shape[0] != m.shape[1]:
+        return False
+    if isinstance(m, DenseMatrix) or hasattr(m, "array"):
+        a = np.asarray(m.array)
+        return float(np.abs(a - a.conj().T).max()) <= tol if a.size else True
+    diff = linear_combine([1.0, -1.0], [m, m.conj_transpose()])
+    return (float(np.abs(diff.values).max()) if diff.nnz else 0.0) <= tol
+
+
+def one_norm_host(m) -> float:
+    """max column abs sum, for host-side validation tolerances only."""
+    if isinstance(m, DenseMatrix) or hasattr(m, "array"):
+        a = np.asarray(m.array)
+        return float(np.abs(a).sum(axis=0).max()) if a.size else 0.0
+    if m.nnz == 0:
+        return 0.0
+    return float(np.bincount(m.col_indices, weights=np.abs(m.values), minlength=m.n_cols).max())
