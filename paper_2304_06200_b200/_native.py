@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libleangrape_b200.so")
+LIB_PATH = os.path.join(_HERE, "_lib_debug" if os.environ.get("LG_DEBUG") else "_lib", "libleangrape_b200.so")
 
 LG_OK = 0
 LG_INVALID_ARG = 1

@@ -14,7 +14,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "_lib")
+OUT = os.path.join(HERE, "_lib" + ("_debug" if os.environ.get("LG_DEBUG") else ""))
 LIB = os.path.join(OUT, "libleangrape_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,6 +26,7 @@ UNITS = {
     "lg_prep.cu": ["-fmad=false"],
     "lg_api.cu": ["-fmad=false"],
     "lg_engine.cu": [],
+    "lg_sweep_cta.cu": ["-DLG_DEBUG"] if os.environ.get("LG_DEBUG") else [],
 }
 
 

@@ -37,6 +37,7 @@ extern "C" void* lg_prep_sparse_kernel();
 extern "C" void* lg_prep_dense_kernel();
 extern "C" void* lg_plans_kernel();
 extern "C" void* lg_gather_kernel();
+extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 
 namespace {
 
@@ -187,6 +188,8 @@ struct lg_problem {
   std::vector<double2> cvals;
   // engine configuration
   bool multi = false;
+  int engine = 0;  // 0 legacy single-CTA, 1 legacy multi-CTA (grid barrier), 2 cta engine
+  int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
   long scratch_per_group = 0;
   std::vector<int> grp_set, grp_t0, grp_nT;
@@ -498,6 +501,10 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.red_cap = p->red_cap;
   E.smem_bytes = p->smem_bytes;
   E.smem_mode = p->smem_mode;
+  E.row_lanes = p->row_lanes;
+  E.cta_Imax = p->cta_Imax;
+  E.grp_T = 1;
+  for (int g = 0; g < p->n_groups; ++g) E.grp_T = std::max(E.grp_T, p->grp_nT[g]);
   E.ip = p->d_ip;
   E.fin = p->d_fin;
   E.run = p->d_run;
@@ -542,7 +549,9 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   const dim3 grid(p->n_groups * p->n_slabs), block(p->threads);
   int rc = LG_OK;
   p->mark(1);
-  if (p->n_groups > 0) rc = launch(lg_forward_kernel(p->multi), grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+  void* fwd = p->engine == 2 ? lg_cta_kernel(0, p->cta_maxr, p->cta_maxc, p->cta_wreg) : lg_forward_kernel(p->multi);
+  void* bwd = p->engine == 2 ? lg_cta_kernel(1, p->cta_maxr, p->cta_maxc, p->cta_wreg) : lg_backward_kernel(p->multi);
+  if (p->n_groups > 0) rc = launch(fwd, grid, block, eargs, p->smem_bytes, p->stream, p->multi);
   if (rc) return rc;
   p->mark(2);
   if (grad && S > 0 && p->n_groups > 0) {
@@ -551,7 +560,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     void* targs[] = {&p->d_trp, &Sv, &Ni, &Tv, &p->d_spec_t0, &p->d_spec_K, &p->d_trsum};
     rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
     if (rc) return rc;
-    rc = launch(lg_backward_kernel(p->multi), grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+    rc = launch(bwd, grid, block, eargs, p->smem_bytes, p->stream, p->multi);
     if (rc) return rc;
   }
   p->mark(3);
@@ -575,6 +584,87 @@ int check_field(lg_problem* p, long N, double dt, const double* amps) {
   return LG_OK;
 }
 
+// CTA engine: one CTA per trajectory (up to 64 groups), everything in shared memory.
+bool configure_cta(lg_problem* p, int nsm, int smem_optin) {
+  (void)nsm;
+  const long d = p->d;
+  int nspec[2] = {0, 0};
+  for (auto& s : p->specs) nspec[s.set]++;
+  const int Imax = std::max({1, nspec[0], nspec[1]});
+  int ksum = 0;
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    ksum += std::max(0, hi - lo);
+  }
+  const int tpg = std::max(1, (ksum + 63) / 64);  // trajectories per group
+  std::vector<int> gset, gt0, gnT;
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    for (int a = lo; a < hi; a += tpg) {
+      gset.push_back(s);
+      gt0.push_back(p->set_t0[s] + a);
+      gnT.push_back(std::min(tpg, hi - a));
+    }
+  }
+  if (gset.size() > 64) return false;
+  const long T = tpg;
+  const long cstate = T * (1 + Imax), cxc = (long)(p->Kc + 1) * T, cmax = std::max(cstate, cxc);
+  const int variants[][2] = {{1, 1}, {1, 2}, {2, 1}, {2, 2}, {1, 4}, {4, 1}};
+  for (auto& v : variants) {
+    const int maxr = v[0], maxc = v[1];
+    const long cs = (cmax + maxc - 1) / maxc;
+    const long rl = 32 * (((d + maxr - 1) / maxr + 31) / 32);
+    const long threads = rl * cs;
+    if (threads > (maxr == 1 ? 512 : 1024)) continue;
+    int wreg = (p->W <= 8 && maxr <= 2 && maxc <= 2) ? 8 : 0;
+    if (std::getenv("LG_CTA_NOWREG")) wreg = 0;
+    const long red_cap = (long)Imax * std::max(p->Kc, 1) * T + 1;
+    long words = red_cap * (rl / 32) + red_cap + 2 * cstate * d + 2 * cmax * d;  // double2 units
+    const long budget = std::min<long>(smem_optin, 227 * 1024) / 16;
+    if (words > budget) continue;
+    int mode = 0;
+    const long a_words = (long)p->W * d + ((long)p->W * d + 1) / 2;
+    if (wreg == 0 && words + a_words <= budget && !std::getenv("LG_CTA_NOASMEM")) {
+      mode |= 4;
+      words += a_words;
+    }
+    const long ac_words = (long)p->Kc * p->Wc * d + ((long)p->Kc * p->Wc * d + 1) / 2;
+    if (words + ac_words <= budget && !std::getenv("LG_CTA_NOACSMEM")) {
+      mode |= 8;
+      words += ac_words;
+    }
+    void* f0 = lg_cta_kernel(0, maxr, maxc, wreg);
+    void* f1 = lg_cta_kernel(1, maxr, maxc, wreg);
+    if (!f0 || !f1) continue;
+    if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(words * 16)) != cudaSuccess ||
+        cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(words * 16)) != cudaSuccess)
+      continue;
+    p->engine = 2;
+    p->multi = false;
+    p->cta_maxr = maxr;
+    p->cta_maxc = maxc;
+    p->cta_wreg = wreg;
+    p->row_lanes = (int)rl;
+    p->cta_Imax = Imax;
+    p->threads = (int)threads;
+    p->n_slabs = 1;
+    p->smem_mode = mode;
+    p->smem_bytes = (int)(words * 16);
+    p->red_cap = (int)red_cap;
+    p->grp_set = gset;
+    p->grp_t0 = gt0;
+    p->grp_nT = gnT;
+    p->n_groups = (int)gset.size();
+    p->live_peak = (int)((2 * cstate + 2 * cmax + T - 1) / T);
+    p->scratch_per_group = 0;
+    p->d_bar = p->mem.alloc<unsigned>(4 * (size_t)std::max(p->n_groups, 1));
+    p->d_scratch = p->mem.alloc<double2>(1);
+    p->d_red = p->mem.alloc<double2>(1);
+    return true;
+  }
+  return false;
+}
+
 // Choose the work decomposition and the shared-memory placement.
 int configure(lg_problem* p) {
   int dev = p->device, nsm = 0, smem_optin = 0;
@@ -582,9 +672,12 @@ int configure(lg_problem* p) {
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const long d = p->d;
   const char* force = std::getenv("LG_ENGINE");
+  const std::string fs = force ? force : "";
   bool multi = d > 4096;
-  if (force && std::string(force) == "multi") multi = true;
-  if (force && std::string(force) == "single") multi = false;
+  if (fs == "multi") multi = true;
+  if (fs == "single" || fs == "legacy") multi = false;
+  if (!multi && fs != "single" && fs != "legacy" && configure_cta(p, nsm, smem_optin)) return LG_OK;
+  if (!g_err.empty() && g_err.rfind("cta:", 0) == 0) g_err.clear();
   int nsets = (p->set_T[0] > 0) + (p->set_T[1] > 0);
   p->grp_set.clear();
   p->grp_t0.clear();

@@ -1,0 +1,560 @@
+// Single-CTA sweep engine: one CTA owns one trajectory group for the whole
+// evaluation (forward and backward sweeps of src/costs.py:269-354, :407-488).
+//
+// Every Taylor term (src/expm.py:345-350) is one fused step over the chain's
+// columns with a FIXED thread <-> (row, column) ownership for the whole chain:
+//   * the Taylor accumulator `cur` of each owned (row, column) stays in registers;
+//   * narrow operators (ELL width <= WREG) keep the thread's rows of A_n in
+//     registers for the whole step; wide ones read A_n from shared memory;
+//   * the term vectors live in shared memory (double-buffered) -> ONE
+//     __syncthreads per Taylor term and no global traffic inside a chain.
+// Thread layout: blockDim = RL row lanes x CS column slots, RL a multiple of 32,
+// so every warp belongs to exactly one column slot and column reductions are
+// warp-shuffle trees (deterministic, fixed order).
+#include "lg_final.cuh"
+#include "lg_types.h"
+
+#ifdef LG_DEBUG
+#include <cstdio>
+__device__ __forceinline__ unsigned lg_dyn_smem() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ double2& lg_smx(double2* sm, long idx, int line) {
+  const long n = lg_dyn_smem() / 16;
+  if (idx < 0 || idx >= n) {
+    printf("LG_DEBUG smem OOB idx=%ld words=%ld line=%d block=%d thread=%d\n", idx, n, line, blockIdx.x, threadIdx.x);
+    return sm[0];
+  }
+  return sm[idx];
+}
+#define SMX(i) lg_smx(sm, (long)(i), __LINE__)
+#else
+#define SMX(i) sm[i]
+#endif
+
+namespace {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cdot(double2 a, double2 b) {  // conj(a) b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// Shared-memory layout (offsets in double2 units), filled by init().
+struct Lay {
+  int red;      // [64] reduction scratch
+  int res;      // [64] reduction results
+  int a;        // A_n [W][d] (smem-A mode)
+  int acols;    // int view: A cols [W][d] (smem-A mode)
+  int ac;       // A_c [Kc][Wc][d] (if in smem) else -1
+  int accols;   // int view
+  int state;    // [T(1+I)][d]   psi | lambda
+  int next;     // [T(1+I)][d]   adjoint results
+  int tb0, tb1; // [Cmax][d]
+};
+
+struct Ctx {
+  const LgEngineArgs* E;
+  int d, T, I, t0, set, trel;
+  int rl, cs, lane, slot;
+  int W, Wc;
+  bool a_smem, ac_smem;
+  const double2* astep;  // global A_n of the current step (global-A mode)
+  Lay L;
+};
+
+template <int MAXR, int MAXC, int WREG>
+struct Regs {
+  double2 cur[MAXC][MAXR];
+  double2 a[MAXR][WREG > 0 ? WREG : 1];
+  int col[MAXR][WREG > 0 ? WREG : 1];
+};
+
+__device__ __forceinline__ int row_of(const Ctx& c, int k) { return c.lane + k * c.rl; }
+
+// One Taylor chain.  mode 0: columns read input column c of `xin` (smem offset,
+// stride d).  mode 1 (aux embedding): columns [0, G*T) are tops for channel
+// gch[c / T] with zero input and bottom partner G*T + c % T; [G*T, (G+1)*T) are
+// bottoms with input xin[t].  Result: cur registers of the owned (row, column)s.
+template <int MAXR, int MAXC, int WREG>
+__device__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int mode, int m, int s, double sgn,
+                      int xin, const int* gch, int G) {
+  const int d = c.d, T = c.T;
+  const int ntop = mode == 1 ? G * T : 0;
+  const int* smi = reinterpret_cast<const int*>(sm);
+  const LgEngineArgs& E = *c.E;
+  // initial accumulator = input
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = c.slot + q * c.cs;
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+      const int i = row_of(c, k);
+      double2 v = make_double2(0.0, 0.0);
+      if (col < C && i < d) {
+        if (mode == 0)
+          v = SMX(xin + col * d + i);
+        else if (col >= ntop)
+          v = SMX(xin + (col - ntop) * d + i);
+      }
+      R.cur[q][k] = v;
+    }
+  }
+  int X = xin, Y = c.L.tb0, Yn = c.L.tb1;
+  bool first = true;
+  for (int si = 0; si < s; ++si) {
+    for (int j = 1; j <= m; ++j) {
+      const double r = sgn * (1.0 / (double)(s * j));
+      const bool last = j == m;
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int col = c.slot + q * c.cs;
+        if (col >= C) continue;
+        const bool top = col < ntop;
+        // input column of this term
+        int xc;
+        if (first && mode == 1)
+          xc = top ? -1 : xin + (col - ntop) * d;
+        else
+          xc = X + col * d;
+        int bc = 0, kch = 0;
+        if (top) {
+          const int t = col % T;
+          kch = gch[col / T];
+          bc = first ? xin + t * d : X + (ntop + t) * d;
+        }
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) {
+          const int i = row_of(c, k);
+          if (i >= d) continue;
+          double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+          if (xc >= 0) {
+            if (WREG > 0) {
+#pragma unroll
+              for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) {
+                if (w < c.W) {
+                  const double2 x = SMX(xc + R.col[k][w]);
+                  const double2 a = R.a[k][w];
+                  double2& acc = (w & 1) ? a1 : a0;
+                  acc.x = fma(a.x, x.x, acc.x);
+                  acc.x = fma(-a.y, x.y, acc.x);
+                  acc.y = fma(a.x, x.y, acc.y);
+                  acc.y = fma(a.y, x.x, acc.y);
+                }
+              }
+            } else {
+              const double2* Ap = c.a_smem ? sm + c.L.a : c.astep;
+              const int* Cp = c.a_smem ? smi + 4 * c.L.acols : E.A_cols;
+              for (int w = 0; w < c.W; ++w) {
+                const int q2 = w * d + i;
+                const double2 x = SMX(xc + Cp[q2]);
+                const double2 a = Ap[q2];
+                double2& acc = (w & 1) ? a1 : a0;
+                acc.x = fma(a.x, x.x, acc.x);
+                acc.x = fma(-a.y, x.y, acc.x);
+                acc.y = fma(a.x, x.y, acc.y);
+                acc.y = fma(a.y, x.x, acc.y);
+              }
+            }
+          }
+          if (top) {
+            const double2* Acp = c.ac_smem ? sm + c.L.ac : E.Ac;
+            const int* Ccp = c.ac_smem ? smi + 4 * c.L.accols : E.Ac_cols;
+            const int base = kch * c.Wc * d + i;
+            for (int w = 0; w < c.Wc; ++w) {
+              const double2 x = SMX(bc + Ccp[base + w * d]);
+              const double2 a = Acp[base + w * d];
+              double2& acc = (w & 1) ? a1 : a0;
+              acc.x = fma(a.x, x.x, acc.x);
+              acc.x = fma(-a.y, x.y, acc.x);
+              acc.y = fma(a.x, x.y, acc.y);
+              acc.y = fma(a.y, x.x, acc.y);
+            }
+          }
+          const double2 tt = make_double2((a0.x + a1.x) * r, (a0.y + a1.y) * r);
+          R.cur[q][k] = cadd(R.cur[q][k], tt);
+          SMX(Y + col * d + i) = last ? R.cur[q][k] : tt;
+        }
+      }
+      __syncthreads();
+      X = Y;
+      const int t_ = Y;
+      Y = Yn;
+      Yn = t_;
+      first = false;
+    }
+  }
+}
+
+// Block reduction of per-thread values v[q] for "virtual columns" vc = map(q):
+// each warp belongs to one column slot; lanes are rows.  out[vc] in smem res.
+__device__ __forceinline__ void red_put(const Ctx& c, double2* sm, int vc, double2 v) {
+  v = warp_sum(v);
+  const int wpc = c.rl / 32;
+  if ((threadIdx.x & 31) == 0) SMX(c.L.red + vc * wpc + (c.lane >> 5)) = v;
+}
+__device__ __forceinline__ void red_finish(const Ctx& c, double2* sm, int nvc) {
+  __syncthreads();
+  const int wpc = c.rl / 32;
+  for (int vc = threadIdx.x; vc < nvc; vc += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = 0; q < wpc; ++q) s = cadd(s, SMX(c.L.red + vc * wpc + q));
+    SMX(c.L.res + vc) = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double2 pen_apply(const LgSpecDev& sp, int d, double2* sm, int psi, int i) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int w = 0; w < sp.pen_W; ++w) {
+    const long q = (long)w * d + i;
+    const double2 x = SMX(psi + sp.pen_cols[q]);
+    const double2 a = sp.pen_vals[q];
+    acc.x = fma(a.x, x.x, acc.x);
+    acc.x = fma(-a.y, x.y, acc.x);
+    acc.y = fma(a.x, x.y, acc.y);
+    acc.y = fma(a.y, x.x, acc.y);
+  }
+  return acc;
+}
+
+template <int MAXR, int MAXC, int WREG>
+__device__ void load_step(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int n) {
+  const LgEngineArgs& E = *c.E;
+  const int d = c.d, W = c.W;
+  const double2* src = E.A + (long)n * W * d;
+  c.astep = src;
+  if (WREG > 0) {
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+      const int i = row_of(c, k);
+#pragma unroll
+      for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) {
+        double2 a = make_double2(0.0, 0.0);
+        int cc = 0;
+        if (i < d && w < W) {
+          a = src[(long)w * d + i];
+          cc = E.A_cols[w * d + i];
+        }
+        R.a[k][w] = a;
+        R.col[k][w] = cc;
+      }
+    }
+  } else if (c.a_smem) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < W * d; q += blockDim.x) SMX(c.L.a + q) = src[q];
+    __syncthreads();
+  }
+}
+
+template <int MAXR, int MAXC, int WREG>
+__device__ void init(Ctx& c, double2* sm, const LgEngineArgs& E) {
+  c.E = &E;
+  c.d = E.d;
+  const int g = blockIdx.x;
+  c.set = E.grp_set[g];
+  c.t0 = E.grp_t0[g];
+  c.T = E.grp_nT[g];
+  c.I = E.set_nspec[c.set];
+  c.trel = c.t0 - E.set_t0[c.set];
+  c.rl = E.row_lanes;
+  c.cs = blockDim.x / c.rl;
+  c.lane = threadIdx.x % c.rl;
+  c.slot = threadIdx.x / c.rl;
+  c.W = E.W;
+  c.Wc = E.Wc;
+  c.a_smem = (E.smem_mode & 4) != 0;
+  c.ac_smem = (E.smem_mode & 8) != 0;
+  const int d = E.d, Tg = E.grp_T;
+  const int cstate = Tg * (1 + E.cta_Imax), cx = (E.Kc + 1) * Tg, cmax = cstate > cx ? cstate : cx;
+  int o = 0;
+  c.L.red = o;
+  o += E.red_cap * (c.rl / 32);
+  c.L.res = o;
+  o += E.red_cap;
+  c.L.a = o;
+  c.L.acols = o + E.W * d;  // int view: offset in double2 * 2 -> handled by 2* in use
+  if (c.a_smem) o += E.W * d + (E.W * d + 1) / 2;
+  c.L.ac = o;
+  c.L.accols = o + E.Kc * E.Wc * d;
+  if (c.ac_smem) o += E.Kc * E.Wc * d + (E.Kc * E.Wc * d + 1) / 2;
+  c.L.state = o;
+  o += cstate * d;
+  c.L.next = o;
+  o += cstate * d;
+  c.L.tb0 = o;
+  o += cmax * d;
+  c.L.tb1 = o;
+  // int views: a double2 offset o is int offset 4 o
+  int* smi = reinterpret_cast<int*>(sm);
+  if (c.a_smem) {
+    for (int q = threadIdx.x; q < E.W * d; q += blockDim.x) smi[4 * c.L.acols + q] = E.A_cols[q];
+  }
+  if (c.ac_smem) {
+    for (int q = threadIdx.x; q < E.Kc * E.Wc * d; q += blockDim.x) {
+      SMX(c.L.ac + q) = E.Ac[q];
+      smi[4 * c.L.accols + q] = E.Ac_cols[q];
+    }
+  }
+  (void)Tg;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------- forward
+template <int MAXR, int MAXC, int WREG>
+__global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_forward(const __grid_constant__ LgEngineArgs E) {
+  extern __shared__ double2 sm[];
+  Ctx c;
+  init<MAXR, MAXC, WREG>(c, sm, E);
+  Regs<MAXR, MAXC, WREG> R;
+  const int d = c.d, T = c.T;
+  const int psi = c.L.state;
+  for (int q = threadIdx.x; q < T * d; q += blockDim.x) SMX(psi + q) = E.psi0[(long)c.t0 * d + q];
+  __syncthreads();
+  int qspec[LG_MAX_SPECS];
+  for (int n = 0; n < E.N; ++n) {
+    const int4 pl = E.plan[(long)n * (E.Kc + 1)];
+    load_step<MAXR, MAXC, WREG>(c, sm, R, n);
+    chain<MAXR, MAXC, WREG>(c, sm, R, T, 0, pl.x, pl.y, 1.0, psi, nullptr, 0);
+    // write back psi_n
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int col = c.slot + q * c.cs;
+#pragma unroll
+      for (int k = 0; k < MAXR; ++k) {
+        const int i = row_of(c, k);
+        if (col < T && i < d) SMX(psi + col * d + i) = R.cur[q][k];
+      }
+    }
+    __syncthreads();
+    const bool final_step = n == E.N - 1;
+    int nq = 0;
+    for (int si = 0; si < c.I; ++si) {
+      const int sidx = E.set_spec[c.set][si];
+      const int kind = E.spec[sidx].kind;
+      if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN || kind == LGK_GATE_RUN ||
+          (final_step && (kind == LGK_STATE_INF || kind == LGK_GATE)))
+        qspec[nq++] = sidx;
+    }
+    if (nq == 0) continue;
+    // per-step scalars: virtual column vc = q * T + t handled by slot (vc % cs)
+    const int nvc = nq * T;
+    for (int vc0 = 0; vc0 < nvc; vc0 += c.cs) {
+      const int vc = vc0 + c.slot;
+      double2 v = make_double2(0.0, 0.0);
+      if (vc < nvc) {
+        const int q = vc / T, t = vc - q * T;
+        const LgSpecDev& sp = E.spec[qspec[q]];
+        for (int i = c.lane; i < d; i += c.rl) {
+          const double2 pv = SMX(psi + t * d + i);
+          if (sp.kind == LGK_STATE_PEN) {
+            v = cadd(v, cdot(pv, pen_apply(sp, d, sm, psi + t * d, i)));
+          } else {
+            const double2 tv = sp.tgt[(long)(c.trel + t) * d + i];
+            v = cadd(v, sp.kind == LGK_STATE_INF ? cdot(pv, tv) : cdot(tv, pv));
+          }
+        }
+      }
+      if (vc0 + c.slot < nvc) red_put(c, sm, vc, v);
+    }
+    red_finish(c, sm, nvc);
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < nq; ++q) {
+        const int sidx = qspec[q];
+        const int kind = E.spec[sidx].kind;
+        for (int t = 0; t < T; ++t) {
+          const double2 r = SMX(c.L.res + q * T + t);
+          const long o = (long)sidx * E.T_total + c.t0 + t;
+          if (kind == LGK_STATE_PEN) {
+            E.run[o] += r.x;
+          } else if (kind == LGK_STATE_RUN) {
+            const double a = hypot(r.x, r.y);
+            E.run[o] += a * a;
+          } else if (kind == LGK_GATE_RUN) {
+            E.trp[((long)sidx * E.N + n) * E.T_total + c.t0 + t] = r;
+          } else {
+            E.fin[o] = r;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < T * d; q += blockDim.x) E.psiN[(long)c.t0 * d + q] = SMX(psi + q);
+}
+
+// ------------------------------------------------------------------------------------------- backward
+template <int MAXR, int MAXC, int WREG>
+__global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_backward(const __grid_constant__ LgEngineArgs E) {
+  extern __shared__ double2 sm[];
+  Ctx c;
+  init<MAXR, MAXC, WREG>(c, sm, E);
+  Regs<MAXR, MAXC, WREG> R;
+  const int d = c.d, T = c.T, I = c.I, Kc = E.Kc, N = E.N;
+  const int st = c.L.state, nx = c.L.next;
+  auto lam = [&](int si, int t) { return T + si * T + t; };  // column index in state/next
+  for (int q = threadIdx.x; q < T * d; q += blockDim.x) SMX(st + q) = E.psiN[(long)c.t0 * d + q];
+  __syncthreads();
+  // ---- costate initialisation (src/costs.py:312-321, :457-460)
+  {
+    const int nvc = I * T;
+    for (int vc0 = 0; vc0 < nvc; vc0 += c.cs) {
+      const int vc = vc0 + c.slot;
+      double2 v = make_double2(0.0, 0.0);
+      if (vc < nvc) {
+        const int si = vc / T, t = vc - si * T;
+        const LgSpecDev& sp = E.spec[E.set_spec[c.set][si]];
+        if (sp.kind == LGK_STATE_RUN)
+          for (int i = c.lane; i < d; i += c.rl) v = cadd(v, cdot(sp.tgt[(long)(c.trel + t) * d + i], SMX(st + t * d + i)));
+        red_put(c, sm, vc, v);
+      }
+    }
+    red_finish(c, sm, nvc);
+    for (int si = 0; si < I; ++si) {
+      const int sidx = E.set_spec[c.set][si];
+      const LgSpecDev& sp = E.spec[sidx];
+      const double2 trN = sp.kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + N - 1] : make_double2(0.0, 0.0);
+      for (int t = 0; t < T; ++t) {
+        const double2 ov = SMX(c.L.res + si * T + t);
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+          double2 v;
+          if (sp.kind == LGK_STATE_PEN) {
+            v = pen_apply(sp, d, sm, st + t * d, i);
+          } else {
+            const double2 tv = sp.tgt[(long)(c.trel + t) * d + i];
+            v = sp.kind == LGK_STATE_RUN ? cmul(tv, ov) : (sp.kind == LGK_GATE_RUN ? cmul(tv, trN) : tv);
+          }
+          SMX(st + lam(si, t) * d + i) = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  int gch[LG_MAX_CHANNELS];
+  for (int n = N - 1; n >= 0; --n) {
+    const int4* pln = E.plan + (long)n * (Kc + 1);
+    const int4 pl = pln[0];
+    load_step<MAXR, MAXC, WREG>(c, sm, R, n);
+    // adjoint chain on [psi | lambda] (src/costs.py:326,342); costates unused at n == 0
+    const int cadj = n > 0 ? T * (1 + I) : T;
+    chain<MAXR, MAXC, WREG>(c, sm, R, cadj, 0, pl.x, pl.y, -1.0, st, nullptr, 0);
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int col = c.slot + q * c.cs;
+#pragma unroll
+      for (int k = 0; k < MAXR; ++k) {
+        const int i = row_of(c, k);
+        if (col < cadj && i < d) SMX(nx + col * d + i) = R.cur[q][k];
+      }
+    }
+    __syncthreads();
+    // derivative products, channels grouped by identical aux plan (src/costs.py:328-339)
+    unsigned done = 0;
+    for (int kc = 0; kc < Kc; ++kc) {
+      if (done & (1u << kc)) continue;
+      const int4 pk = pln[1 + kc];
+      int G = 0;
+      for (int k2 = kc; k2 < Kc; ++k2) {
+        const int4 p2 = pln[1 + k2];
+        if (!(done & (1u << k2)) && p2.x == pk.x && p2.y == pk.y) {
+          gch[G++] = k2;
+          done |= 1u << k2;
+        }
+      }
+      const int caux = (G + 1) * T;
+      chain<MAXR, MAXC, WREG>(c, sm, R, caux, 1, pk.x, pk.y, 1.0, nx, gch, G);
+      // <lambda_(si,t) | D_(k,t)>: the owner of top column (g, t) holds D in registers
+      const int ntop = G * T;
+      for (int si = 0; si < I; ++si) {
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q) {
+          const int col = c.slot + q * c.cs;
+          if (col >= ntop) continue;
+          const int t = col % T;
+          double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < MAXR; ++k) {
+            const int i = row_of(c, k);
+            if (i < d) v = cadd(v, cdot(SMX(st + lam(si, t) * d + i), R.cur[q][k]));
+          }
+          red_put(c, sm, si * ntop + col, v);
+        }
+      }
+      red_finish(c, sm, I * ntop);
+      if (threadIdx.x < I * ntop) {
+        const int vc = threadIdx.x;
+        const int si = vc / ntop, col = vc - si * ntop;
+        const int t = col % T, gi = col / T;
+        const int sidx = E.set_spec[c.set][si];
+        E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + c.t0 + t] = SMX(c.L.res + vc);
+      }
+      __syncthreads();
+    }
+    if (n == 0) break;
+    // costate sources at psi_{n-1} (src/costs.py:341-353, :474-479)
+    {
+      const int nvc = I * T;
+      bool any_run = false;
+      for (int si = 0; si < I; ++si) any_run |= E.spec[E.set_spec[c.set][si]].kind == LGK_STATE_RUN;
+      if (any_run) {
+        for (int vc0 = 0; vc0 < nvc; vc0 += c.cs) {
+          const int vc = vc0 + c.slot;
+          double2 v = make_double2(0.0, 0.0);
+          if (vc < nvc) {
+            const int si = vc / T, t = vc - si * T;
+            const LgSpecDev& sp = E.spec[E.set_spec[c.set][si]];
+            if (sp.kind == LGK_STATE_RUN)
+              for (int i = c.lane; i < d; i += c.rl)
+                v = cadd(v, cdot(sp.tgt[(long)(c.trel + t) * d + i], SMX(nx + t * d + i)));
+            red_put(c, sm, vc, v);
+          }
+        }
+        red_finish(c, sm, nvc);
+      }
+      for (int si = 0; si < I; ++si) {
+        const int sidx = E.set_spec[c.set][si];
+        const LgSpecDev& sp = E.spec[sidx];
+        const double2 tr = sp.kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
+        for (int t = 0; t < T; ++t) {
+          const double2 ov = any_run ? SMX(c.L.res + si * T + t) : make_double2(0.0, 0.0);
+          const int col = lam(si, t);
+          for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            double2 v = SMX(nx + col * d + i);
+            if (sp.kind == LGK_STATE_PEN)
+              v = cadd(v, pen_apply(sp, d, sm, nx + t * d, i));
+            else if (sp.kind == LGK_STATE_RUN)
+              v = cadd(v, cmul(sp.tgt[(long)(c.trel + t) * d + i], ov));
+            else if (sp.kind == LGK_GATE_RUN)
+              v = cadd(v, cmul(sp.tgt[(long)(c.trel + t) * d + i], tr));
+            SMX(st + col * d + i) = v;
+          }
+        }
+      }
+      for (int q = threadIdx.x; q < T * d; q += blockDim.x) SMX(st + q) = SMX(nx + q);
+      __syncthreads();
+    }
+  }
+}
+
+#define LG_CTA_VARIANTS(X) X(1, 1, 8) X(1, 1, 0) X(1, 2, 8) X(1, 2, 0) X(2, 1, 8) X(2, 1, 0) X(4, 1, 0) X(2, 2, 0) X(1, 4, 0)
+
+extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg) {
+#define LG_PICK(R_, C_, W_)                                                                        \
+  if (maxr == R_ && maxc == C_ && wreg == W_)                                                      \
+    return backward ? (void*)lg_k_cta_backward<R_, C_, W_> : (void*)lg_k_cta_forward<R_, C_, W_>;
+  LG_CTA_VARIANTS(LG_PICK)
+#undef LG_PICK
+  return nullptr;
+}

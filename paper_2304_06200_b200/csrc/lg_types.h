@@ -82,7 +82,9 @@ struct LgEngineArgs {
   double2* red;             // per group [2][red_cap][n_slabs]
   int red_cap;
   int smem_bytes;           // dynamic shared memory provided
-  int smem_mode;            // bit0: all state buffers in smem; bit1: term buffers in smem; bit2: A_n in smem
+  int smem_mode;            // legacy engine: bit0 state in smem, bit1 term buffers, bit2 A_n; cta engine: bit2 A_n, bit3 A_c
+  int row_lanes;            // cta engine: row lanes (multiple of 32); blockDim = row_lanes x column slots
+  int cta_Imax;             // cta engine: max specs per set (state layout stride)
   // raw outputs (indexed by global trajectory)
   double2* ip;              // [N][n_specs][Kc][T_total]
   double2* fin;             // [n_specs][T_total]
