@@ -27,6 +27,7 @@ UNITS = {
     "lg_api.cu": ["-fmad=false"],
     "lg_engine.cu": [],
     "lg_sweep_cta.cu": ["-DLG_DEBUG"] if os.environ.get("LG_DEBUG") else [],
+    "lg_dense.cu": [],
 }
 
 
@@ -47,19 +48,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(OUT, exist_ok=True)
-    objs = []
-    for unit, flags in UNITS.items():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_unit(item):
+        unit, flags = item
         obj = os.path.join(OUT, unit.replace(".cu", ".o"))
         cmd = [NVCC, *COMMON, *flags, "-c", os.path.join(SRC, unit), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed for {unit}")
-        if verbose:
-            sys.stderr.write(r.stderr)
         with open(os.path.join(OUT, unit + ".ptxas.log"), "w") as fh:
             fh.write(r.stderr)
-        objs.append(obj)
+        return unit, obj, r
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
+        for unit, obj, r in ex.map(compile_unit, UNITS.items()):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed for {unit}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,0 +1,285 @@
+// Dense large-d path (DenseMatrix generators, e.g. config 5: d = 4096, K = 64).
+//
+// Each Taylor term (src/expm.py:345-350 with DenseMatrix.matvec, src/sparse.py:193-199)
+// is ONE complex FP64 GEMM over all columns of the chain on the FP64 tensor
+// pipe (mma.sync.aligned.m8n8k4.f64 -> SASS DMMA; sm_100a has no tcgen05 f64
+// kind), with the Taylor scale-and-accumulate fused into the epilogue:
+//     t = (A X) (sgn / (s j));  cur += t;  T_out = last ? cur : t.
+// A is stored planar (Ar, Ai), column-major; X / cur / T are interleaved
+// double2, column-major (column = one state vector).  The complex product is
+// four real MMAs per fragment pair: Yr += Ar Xr + Ai (-Xi), Yi += Ar Xi + Ai Xr.
+// An operand may be the concatenation of two segments (the aux embedding's
+// top block [A | A_c] [top; bottom], src/derivatives.py:154-164).
+#include <cuda_runtime.h>
+
+#include "lg_types.h"
+
+namespace {
+
+constexpr int BM = 64, BN = 16, BK = 16, SA = BM + 8, SX = BN + 1;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+}  // namespace
+
+struct LgGemmSeg {
+  const double* Ar;  // column-major, element (i, k) at k * lda + i
+  const double* Ai;
+  int lda;
+  const double2* X;  // column-major, element (k, c) at c * ldx + k
+  int ldx;
+  int K;
+};
+
+struct LgGemmArgs {
+  int M, C;
+  LgGemmSeg seg[2];
+  int nseg;
+  const double2* xin;  // cur initialisation on the first term (nullptr: zero)
+  int ldxin;
+  double2* cur;
+  int ldc;
+  double2* tout;
+  int ldt;
+  double r;
+  int first, last;
+};
+
+// grid (ceil(C / BN), ceil(M / BM)); 128 threads = 4 warps, each a 16 x 16 tile.
+extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
+  __shared__ __align__(16) double sAr[2][BK][SA];
+  __shared__ __align__(16) double sAi[2][BK][SA];
+  __shared__ double sXr[2][BK][SX];
+  __shared__ double sXi[2][BK][SX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int M = G.M, C = G.C;
+  double yr[2][2][2], yi[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) yr[a][b][0] = yr[a][b][1] = yi[a][b][0] = yi[a][b][1] = 0.0;
+
+  // flattened k-tiles over the segments
+  int tiles0 = (G.seg[0].K + BK - 1) / BK;
+  int total = tiles0 + (G.nseg > 1 ? (G.seg[1].K + BK - 1) / BK : 0);
+  const bool full_m = (m0 + BM <= M);
+
+  auto load_tile = [&](int t, int buf, double2* xreg) {
+    const LgGemmSeg& S = G.seg[t < tiles0 ? 0 : 1];
+    const int k0 = (t < tiles0 ? t : t - tiles0) * BK;
+    // A: BK columns x BM rows per plane; 16-byte chunks: BK * BM / 2 per plane
+#pragma unroll
+    for (int q = 0; q < (BK * BM / 2) / 128; ++q) {
+      const int chunk = tid + q * 128;
+      const int kk = chunk / (BM / 2), mm = (chunk % (BM / 2)) * 2;
+      const int k = k0 + kk, m = m0 + mm;
+      if (k < S.K && full_m) {
+        cp_async16(&sAr[buf][kk][mm], S.Ar + (long)k * S.lda + m);
+        cp_async16(&sAi[buf][kk][mm], S.Ai + (long)k * S.lda + m);
+      } else {
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = k < S.K && m + e < M;
+          sAr[buf][kk][mm + e] = ok ? S.Ar[(long)k * S.lda + m + e] : 0.0;
+          sAi[buf][kk][mm + e] = ok ? S.Ai[(long)k * S.lda + m + e] : 0.0;
+        }
+      }
+    }
+    // X: BK x BN complex, into registers (stored to smem after the current compute)
+#pragma unroll
+    for (int q = 0; q < (BK * BN) / 128; ++q) {
+      const int e = tid + q * 128;
+      const int nn = e / BK, kk = e % BK;
+      const int k = k0 + kk, n = n0 + nn;
+      xreg[q] = (k < S.K && n < C) ? S.X[(long)n * S.ldx + k] : make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+  };
+  auto store_x = [&](int buf, const double2* xreg) {
+#pragma unroll
+    for (int q = 0; q < (BK * BN) / 128; ++q) {
+      const int e = tid + q * 128;
+      const int nn = e / BK, kk = e % BK;
+      sXr[buf][kk][nn] = xreg[q].x;
+      sXi[buf][kk][nn] = xreg[q].y;
+    }
+  };
+
+  double2 xreg[(BK * BN) / 128];
+  if (total > 0) {
+    load_tile(0, 0, xreg);
+    store_x(0, xreg);
+  }
+  for (int t = 0; t < total; ++t) {
+    const int buf = t & 1;
+    cp_async_wait0();
+    __syncthreads();
+    if (t + 1 < total) load_tile(t + 1, buf ^ 1, xreg);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int ka = kk + (lane & 3);
+      double ar[2], ai[2], xr[2], xi[2], nxi[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int m = warp * 16 + mt * 8 + (lane >> 2);
+        ar[mt] = sAr[buf][ka][m];
+        ai[mt] = sAi[buf][ka][m];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int n = nt * 8 + (lane >> 2);
+        xr[nt] = sXr[buf][ka][n];
+        xi[nt] = sXi[buf][ka][n];
+        nxi[nt] = -xi[nt];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(yr[mt][nt][0], yr[mt][nt][1], ar[mt], xr[nt]);
+          dmma(yr[mt][nt][0], yr[mt][nt][1], ai[mt], nxi[nt]);
+          dmma(yi[mt][nt][0], yi[mt][nt][1], ar[mt], xi[nt]);
+          dmma(yi[mt][nt][0], yi[mt][nt][1], ai[mt], xr[nt]);
+        }
+    }
+    if (t + 1 < total) {
+      __syncthreads();  // everyone done reading sX[buf ^ 1] of tile t - 1
+      store_x(buf ^ 1, xreg);
+    }
+  }
+  // fused Taylor epilogue
+  const double r = G.r;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
+        const int n = n0 + nt * 8 + 2 * (lane & 3) + v;
+        if (m >= M || n >= C) continue;
+        const double2 tt = make_double2(yr[mt][nt][v] * r, yi[mt][nt][v] * r);
+        double2 base;
+        if (G.first)
+          base = G.xin ? G.xin[(long)n * G.ldxin + m] : make_double2(0.0, 0.0);
+        else
+          base = G.cur[(long)n * G.ldc + m];
+        const double2 cu = make_double2(base.x + tt.x, base.y + tt.y);
+        G.cur[(long)n * G.ldc + m] = cu;
+        G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
+      }
+}
+
+// A_n = -i dt (H_s + sum_c a_c h_c), planar column-major, same operand order as
+// linear_combine (src/sparse.py:325-334) and scaled (src/sparse.py:226-227).
+extern "C" __global__ void lg_k_dense_form(const double2* hs, const double2* const* hc, const double* amps, int Kc,
+                                           double dt, long count, double* Ar, double* Ai) {
+  for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (long)gridDim.x * blockDim.x) {
+    double hr = 0.0 + hs[q].x, hi = 0.0 + hs[q].y;
+    for (int c = 0; c < Kc; ++c) {
+      const double a = amps[c];
+      if (a == 0.0) continue;
+      const double2 v = hc[c][q];
+      hr = __dadd_rn(hr, __dmul_rn(v.x, a));
+      hi = __dadd_rn(hi, __dmul_rn(v.y, a));
+    }
+    Ar[q] = __dmul_rn(dt, hi);
+    Ai[q] = -__dmul_rn(dt, hr);
+  }
+}
+
+// Deterministic dot products <u_p | v_p> = sum_i conj(u_p[i]) v_p[i] for a list of
+// column pairs (one CTA per pair, fixed-order tree).  mode bit0: conjugate-free
+// variant not needed; out[p] written.
+struct LgDotArgs {
+  int d, n;
+  const double2* u[64];
+  const double2* v[64];
+  double2* out[64];
+};
+extern "C" __global__ void lg_k_dots(const __grid_constant__ LgDotArgs D) {
+  __shared__ double2 red[32];
+  const int p = blockIdx.x;
+  if (p >= D.n) return;
+  const double2* u = D.u[p];
+  const double2* v = D.v[p];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < D.d; i += blockDim.x) {
+    const double2 a = u[i], b = v[i];
+    acc.x += a.x * b.x + a.y * b.y;
+    acc.y += a.x * b.y - a.y * b.x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s.x += red[w].x, s.y += red[w].y;
+    *D.out[p] = s;
+  }
+}
+
+// y[c] = O x[c] for an ELL operator over several columns; optionally y += (mode 1)
+struct LgEllArgs {
+  int d, W, ncol, accumulate;
+  const int* cols;
+  const double2* vals;
+  const double2* x[64];
+  double2* y[64];
+};
+extern "C" __global__ void lg_k_ell_apply(const __grid_constant__ LgEllArgs A) {
+  const int c = blockIdx.y;
+  const double2* x = A.x[c];
+  double2* y = A.y[c];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.d; i += gridDim.x * blockDim.x) {
+    double2 acc = A.accumulate ? y[i] : make_double2(0.0, 0.0);
+    for (int w = 0; w < A.W; ++w) {
+      const double2 a = A.vals[(long)w * A.d + i], b = x[A.cols[(long)w * A.d + i]];
+      acc.x += a.x * b.x - a.y * b.y;
+      acc.y += a.x * b.y + a.y * b.x;
+    }
+    y[i] = acc;
+  }
+}
+
+// y[c] = alpha_c * u[c] (+ y[c] when accumulate): costate initialisation / sources.
+struct LgAxpyArgs {
+  int d, ncol;
+  const double2* u[64];
+  double2* y[64];
+  double2 alpha[64];
+  const double2* alpha_ptr[64];  // optional device scalar multiplier (nullptr: use alpha)
+  int accumulate[64];
+};
+extern "C" __global__ void lg_k_axpy(const __grid_constant__ LgAxpyArgs A) {
+  const int c = blockIdx.y;
+  const double2* u = A.u[c];
+  double2* y = A.y[c];
+  const double2 al = A.alpha_ptr[c] ? *A.alpha_ptr[c] : A.alpha[c];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.d; i += gridDim.x * blockDim.x) {
+    const double2 v = u[i];
+    double2 t = make_double2(al.x * v.x - al.y * v.y, al.x * v.y + al.y * v.x);
+    if (A.accumulate[c]) t.x += y[i].x, t.y += y[i].y;
+    y[i] = t;
+  }
+}
+
+extern "C" void* lg_zgemm_kernel() { return (void*)lg_k_zgemm_taylor; }
+extern "C" void* lg_dense_form_kernel() { return (void*)lg_k_dense_form; }
+extern "C" void* lg_dots_kernel() { return (void*)lg_k_dots; }
+extern "C" void* lg_ell_kernel() { return (void*)lg_k_ell_apply; }
+extern "C" void* lg_axpy_kernel() { return (void*)lg_k_axpy; }

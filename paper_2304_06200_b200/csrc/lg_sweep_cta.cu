@@ -14,6 +14,8 @@
 #include "lg_final.cuh"
 #include "lg_types.h"
 
+extern __shared__ double2 lg_smem[];
+
 #ifdef LG_DEBUG
 #include <cstdio>
 __device__ __forceinline__ unsigned lg_dyn_smem() {
@@ -29,9 +31,9 @@ __device__ __forceinline__ double2& lg_smx(double2* sm, long idx, int line) {
   }
   return sm[idx];
 }
-#define SMX(i) lg_smx(sm, (long)(i), __LINE__)
+#define SMX(i) lg_smx(lg_smem, (long)(i), __LINE__)
 #else
-#define SMX(i) sm[i]
+#define SMX(i) lg_smem[i]
 #endif
 
 namespace {
@@ -55,6 +57,7 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
 struct Lay {
   int red;      // [64] reduction scratch
   int res;      // [64] reduction results
+  int rt;       // [64] 1/(s j) table (x component)
   int a;        // A_n [W][d] (smem-A mode)
   int acols;    // int view: A cols [W][d] (smem-A mode)
   int ac;       // A_c [Kc][Wc][d] (if in smem) else -1
@@ -74,27 +77,70 @@ struct Ctx {
   Lay L;
 };
 
+// WREG > 0: the operator has exactly WREG stored slots per row (ELL width) and
+// the thread's rows of A_n live in registers; WREG == 0: A_n read from memory.
 template <int MAXR, int MAXC, int WREG>
 struct Regs {
   double2 cur[MAXC][MAXR];
   double2 a[MAXR][WREG > 0 ? WREG : 1];
   int col[MAXR][WREG > 0 ? WREG : 1];
+  double2 ac[MAXC][MAXR][2];  // control-generator row of a top column (Wc <= 2)
+  int accol[MAXC][MAXR][2];
 };
 
 __device__ __forceinline__ int row_of(const Ctx& c, int k) { return c.lane + k * c.rl; }
 
-// One Taylor chain.  mode 0: columns read input column c of `xin` (smem offset,
-// stride d).  mode 1 (aux embedding): columns [0, G*T) are tops for channel
-// gch[c / T] with zero input and bottom partner G*T + c % T; [G*T, (G+1)*T) are
-// bottoms with input xin[t].  Result: cur registers of the owned (row, column)s.
+__device__ __forceinline__ void cmac(double2& p, double2& q, double2 a, double2 x) {
+  // p accumulates (a.x x.x, a.x x.y), q accumulates (-a.y x.y, a.y x.x): two
+  // independent dependency chains per complex product.
+  p.x = fma(a.x, x.x, p.x);
+  p.y = fma(a.x, x.y, p.y);
+  q.x = fma(-a.y, x.y, q.x);
+  q.y = fma(a.y, x.x, q.y);
+}
+
+// One Taylor chain.  mode 0: column c's input is column c of `xin` (smem
+// offset, stride d).  mode 1 (aux embedding): columns [0, G*T) are tops for
+// channel gch[c / T] with zero input and bottom partner G*T + c % T; columns
+// [G*T, (G+1)*T) are bottoms with input xin[t].  The input is first staged into
+// the term buffer so every term reads the same way; everything that does not
+// change from term to term (offsets, control rows, 1/(s j)) is hoisted.
+// Result: the cur registers of the owned (row, column)s.
 template <int MAXR, int MAXC, int WREG>
-__device__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int mode, int m, int s, double sgn,
-                      int xin, const int* gch, int G) {
-  const int d = c.d, T = c.T;
+__device__ __forceinline__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int mode, int m, int s,
+                                      double sgn, int xin, const int* gch, int G) {
+  const int d = c.d, T = c.T, Wc = c.Wc, W = c.W;
   const int ntop = mode == 1 ? G * T : 0;
-  const int* smi = reinterpret_cast<const int*>(sm);
+  const int* smi = reinterpret_cast<const int*>(lg_smem);
   const LgEngineArgs& E = *c.E;
-  // initial accumulator = input
+  const double2* Acp = c.ac_smem ? lg_smem + c.L.ac : E.Ac;
+  const int* Ccp = c.ac_smem ? smi + 4 * c.L.accols : E.Ac_cols;
+  const double2* Ap = c.a_smem ? lg_smem + c.L.a : c.astep;
+  const int* Cp = c.a_smem ? smi + 4 * c.L.acols : E.A_cols;
+  const bool acreg = Wc <= 2;
+  int coff[MAXC], poff[MAXC], kbase[MAXC];
+  bool own[MAXC], top[MAXC];
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = c.slot + q * c.cs;
+    own[q] = col < C;
+    top[q] = own[q] && col < ntop;
+    coff[q] = col * d;
+    const int t = top[q] ? col % T : 0;
+    poff[q] = (ntop + t) * d;
+    kbase[q] = top[q] ? gch[col / T] * Wc * d : 0;
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+      const int i = row_of(c, k);
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const bool on = top[q] && acreg && i < d && w < Wc;
+        R.ac[q][k][w] = on ? Acp[kbase[q] + w * d + i] : make_double2(0.0, 0.0);
+        R.accol[q][k][w] = on ? Ccp[kbase[q] + w * d + i] : 0;
+      }
+    }
+  }
+  // stage the input into tb0 and the accumulators; 1/(s j) table
 #pragma unroll
   for (int q = 0; q < MAXC; ++q) {
     const int col = c.slot + q * c.cs;
@@ -102,97 +148,64 @@ __device__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int
     for (int k = 0; k < MAXR; ++k) {
       const int i = row_of(c, k);
       double2 v = make_double2(0.0, 0.0);
-      if (col < C && i < d) {
+      if (own[q] && i < d) {
         if (mode == 0)
           v = SMX(xin + col * d + i);
-        else if (col >= ntop)
+        else if (!top[q])
           v = SMX(xin + (col - ntop) * d + i);
+        SMX(c.L.tb0 + coff[q] + i) = v;
       }
       R.cur[q][k] = v;
     }
   }
-  int X = xin, Y = c.L.tb0, Yn = c.L.tb1;
-  bool first = true;
+  if (threadIdx.x < m) SMX(c.L.rt + threadIdx.x).x = sgn * (1.0 / (double)(s * (threadIdx.x + 1)));
+  __syncthreads();
+  int X = c.L.tb0, Y = c.L.tb1;
+  const int rt = c.L.rt;
+  int rows[MAXR];
+#pragma unroll
+  for (int k = 0; k < MAXR; ++k) rows[k] = row_of(c, k);
   for (int si = 0; si < s; ++si) {
     for (int j = 1; j <= m; ++j) {
-      const double r = sgn * (1.0 / (double)(s * j));
+      const double r = SMX(rt + j - 1).x;
       const bool last = j == m;
 #pragma unroll
       for (int q = 0; q < MAXC; ++q) {
-        const int col = c.slot + q * c.cs;
-        if (col >= C) continue;
-        const bool top = col < ntop;
-        // input column of this term
-        int xc;
-        if (first && mode == 1)
-          xc = top ? -1 : xin + (col - ntop) * d;
-        else
-          xc = X + col * d;
-        int bc = 0, kch = 0;
-        if (top) {
-          const int t = col % T;
-          kch = gch[col / T];
-          bc = first ? xin + t * d : X + (ntop + t) * d;
-        }
+        if (!own[q]) continue;
+        const int xc = X + coff[q];
 #pragma unroll
         for (int k = 0; k < MAXR; ++k) {
-          const int i = row_of(c, k);
+          const int i = rows[k];
           if (i >= d) continue;
-          double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-          if (xc >= 0) {
-            if (WREG > 0) {
+          double2 p = make_double2(0.0, 0.0), pq = make_double2(0.0, 0.0);
+          if (WREG > 0) {
 #pragma unroll
-              for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) {
-                if (w < c.W) {
-                  const double2 x = SMX(xc + R.col[k][w]);
-                  const double2 a = R.a[k][w];
-                  double2& acc = (w & 1) ? a1 : a0;
-                  acc.x = fma(a.x, x.x, acc.x);
-                  acc.x = fma(-a.y, x.y, acc.x);
-                  acc.y = fma(a.x, x.y, acc.y);
-                  acc.y = fma(a.y, x.x, acc.y);
-                }
-              }
+            for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) cmac(p, pq, R.a[k][w], SMX(xc + R.col[k][w]));
+          } else {
+            for (int w = 0; w < W; ++w) {
+              const int q2 = w * d + i;
+              cmac(p, pq, Ap[q2], SMX(xc + Cp[q2]));
+            }
+          }
+          if (top[q]) {
+            const int bc = X + poff[q];
+            if (acreg) {
+              cmac(p, pq, R.ac[q][k][0], SMX(bc + R.accol[q][k][0]));
+              cmac(p, pq, R.ac[q][k][1], SMX(bc + R.accol[q][k][1]));
             } else {
-              const double2* Ap = c.a_smem ? sm + c.L.a : c.astep;
-              const int* Cp = c.a_smem ? smi + 4 * c.L.acols : E.A_cols;
-              for (int w = 0; w < c.W; ++w) {
-                const int q2 = w * d + i;
-                const double2 x = SMX(xc + Cp[q2]);
-                const double2 a = Ap[q2];
-                double2& acc = (w & 1) ? a1 : a0;
-                acc.x = fma(a.x, x.x, acc.x);
-                acc.x = fma(-a.y, x.y, acc.x);
-                acc.y = fma(a.x, x.y, acc.y);
-                acc.y = fma(a.y, x.x, acc.y);
-              }
+              const int base = kbase[q] + i;
+              for (int w = 0; w < Wc; ++w) cmac(p, pq, Acp[base + w * d], SMX(bc + Ccp[base + w * d]));
             }
           }
-          if (top) {
-            const double2* Acp = c.ac_smem ? sm + c.L.ac : E.Ac;
-            const int* Ccp = c.ac_smem ? smi + 4 * c.L.accols : E.Ac_cols;
-            const int base = kch * c.Wc * d + i;
-            for (int w = 0; w < c.Wc; ++w) {
-              const double2 x = SMX(bc + Ccp[base + w * d]);
-              const double2 a = Acp[base + w * d];
-              double2& acc = (w & 1) ? a1 : a0;
-              acc.x = fma(a.x, x.x, acc.x);
-              acc.x = fma(-a.y, x.y, acc.x);
-              acc.y = fma(a.x, x.y, acc.y);
-              acc.y = fma(a.y, x.x, acc.y);
-            }
-          }
-          const double2 tt = make_double2((a0.x + a1.x) * r, (a0.y + a1.y) * r);
+          const double2 tt = make_double2((p.x + pq.x) * r, (p.y + pq.y) * r);
           R.cur[q][k] = cadd(R.cur[q][k], tt);
-          SMX(Y + col * d + i) = last ? R.cur[q][k] : tt;
+          SMX(Y + coff[q] + i) = last ? R.cur[q][k] : tt;
         }
       }
       __syncthreads();
+      const int t_ = X;
       X = Y;
-      const int t_ = Y;
-      Y = Yn;
-      Yn = t_;
-      first = false;
+      Y = t_;
     }
   }
 }
@@ -243,7 +256,7 @@ __device__ void load_step(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int n)
       for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) {
         double2 a = make_double2(0.0, 0.0);
         int cc = 0;
-        if (i < d && w < W) {
+        if (i < d) {
           a = src[(long)w * d + i];
           cc = E.A_cols[w * d + i];
         }
@@ -283,6 +296,8 @@ __device__ void init(Ctx& c, double2* sm, const LgEngineArgs& E) {
   o += E.red_cap * (c.rl / 32);
   c.L.res = o;
   o += E.red_cap;
+  c.L.rt = o;
+  o += 64;
   c.L.a = o;
   c.L.acols = o + E.W * d;  // int view: offset in double2 * 2 -> handled by 2* in use
   if (c.a_smem) o += E.W * d + (E.W * d + 1) / 2;
@@ -297,7 +312,7 @@ __device__ void init(Ctx& c, double2* sm, const LgEngineArgs& E) {
   o += cmax * d;
   c.L.tb1 = o;
   // int views: a double2 offset o is int offset 4 o
-  int* smi = reinterpret_cast<int*>(sm);
+  int* smi = reinterpret_cast<int*>(lg_smem);
   if (c.a_smem) {
     for (int q = threadIdx.x; q < E.W * d; q += blockDim.x) smi[4 * c.L.acols + q] = E.A_cols[q];
   }
@@ -315,7 +330,7 @@ __device__ void init(Ctx& c, double2* sm, const LgEngineArgs& E) {
 // ------------------------------------------------------------------------------------------- forward
 template <int MAXR, int MAXC, int WREG>
 __global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_forward(const __grid_constant__ LgEngineArgs E) {
-  extern __shared__ double2 sm[];
+  double2* sm = lg_smem;
   Ctx c;
   init<MAXR, MAXC, WREG>(c, sm, E);
   Regs<MAXR, MAXC, WREG> R;
@@ -398,7 +413,7 @@ __global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_forward(co
 // ------------------------------------------------------------------------------------------- backward
 template <int MAXR, int MAXC, int WREG>
 __global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_backward(const __grid_constant__ LgEngineArgs E) {
-  extern __shared__ double2 sm[];
+  double2* sm = lg_smem;
   Ctx c;
   init<MAXR, MAXC, WREG>(c, sm, E);
   Regs<MAXR, MAXC, WREG> R;
@@ -548,7 +563,9 @@ __global__ void __launch_bounds__(MAXR == 1 ? 512 : 1024, 1) lg_k_cta_backward(c
   }
 }
 
-#define LG_CTA_VARIANTS(X) X(1, 1, 8) X(1, 1, 0) X(1, 2, 8) X(1, 2, 0) X(2, 1, 8) X(2, 1, 0) X(4, 1, 0) X(2, 2, 0) X(1, 4, 0)
+#define LG_CTA_W(X, R_, C_) X(R_, C_, 1) X(R_, C_, 2) X(R_, C_, 3) X(R_, C_, 4) X(R_, C_, 5) X(R_, C_, 6) X(R_, C_, 7) X(R_, C_, 8) X(R_, C_, 9)
+#define LG_CTA_VARIANTS(X) LG_CTA_W(X, 1, 1) LG_CTA_W(X, 1, 2) LG_CTA_W(X, 2, 1) \
+  X(1, 1, 0) X(1, 2, 0) X(2, 1, 0) X(4, 1, 0) X(2, 2, 0) X(1, 4, 0)
 
 extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg) {
 #define LG_PICK(R_, C_, W_)                                                                        \

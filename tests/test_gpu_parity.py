@@ -216,3 +216,14 @@ def test_optimizer_decreases_cost():
     tr = grape_optimize(case.problem, case.terms, case.field, OptimizerConfig(max_iters=4, eta0=0.05))
     costs = [r.cost for r in tr.records]
     assert len(costs) >= 2 and all(b <= a for a, b in zip(costs, costs[1:]))
+
+
+def test_c5_prefix_dense_dmma():
+    """config 5 (dense d=4096, DMMA GEMM path): N'=4 steps, K'=4 of the 64 transfers."""
+    z = G.load("c5")
+    case = models.build_case("c5", n_steps=int(z["amps"].shape[0]), n_states=int(z["k_sub"]))
+    assert np.sum(np.abs(case.problem.h_static.array)) == float(z["hs_checksum"])
+    _check(composite_grad(case.problem, case.field, case.terms), z["cost"], z["grad"])
+    a8 = ControlField(8, 1, float(z["dt"]), models.controls(105, 1000, 1, 1.0)[:8])
+    t = NativeProblem(case.problem, case.terms, initial_states=case.problem.initial_state).plan_table(a8)
+    _plans_equal(t, z)
