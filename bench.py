@@ -323,9 +323,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=None,
+                    help="CPU seconds per reference sample (default: ~100 s over all steps)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.ref_budget is None:
+        args.ref_budget = 12.0 if args.impl == "ours" else max(2.0, 100.0 / (args.steps + args.warmup))
     if args.impl == "reference":
         run_reference(args)
     else:

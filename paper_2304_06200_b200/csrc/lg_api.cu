@@ -39,6 +39,8 @@ extern "C" void* lg_plans_kernel();
 extern "C" void* lg_gather_kernel();
 extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 extern "C" void* lg_zgemm_kernel();
+extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
+extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp);
 extern "C" void* lg_dense_form_kernel();
 extern "C" void* lg_dots_kernel();
 extern "C" void* lg_ell_kernel();
@@ -247,6 +249,7 @@ struct lg_problem {
   double dense_dt = NAN;
   std::vector<double2*> d_hc_dense_host;
   int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
+  int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
   long scratch_per_group = 0;
   std::vector<int> grp_set, grp_t0, grp_nT;
@@ -1025,7 +1028,16 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   p->mark(1);
   void* fwd = p->engine == 2 ? lg_cta_kernel(0, p->cta_maxr, p->cta_maxc, p->cta_wreg) : lg_forward_kernel(p->multi);
   void* bwd = p->engine == 2 ? lg_cta_kernel(1, p->cta_maxr, p->cta_maxc, p->cta_wreg) : lg_backward_kernel(p->multi);
-  if (p->n_groups > 0) rc = launch(fwd, grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+  int fsm = p->smem_bytes, bsm = p->smem_bytes;
+  dim3 bblock = block;
+  if (p->engine == 4) {
+    fwd = lg_ws_kernel(0, p->W, p->ws_rpl);
+    bwd = lg_ws_kernel(1, p->W, p->ws_rpl);
+    fsm = p->ws_fwd_smem;
+    bsm = p->ws_bwd_smem;
+    bblock = dim3(p->ws_bwd_threads);
+  }
+  if (p->n_groups > 0) rc = launch(fwd, grid, block, eargs, fsm, p->stream, p->multi);
   if (rc) return rc;
   p->mark(2);
   if (grad && S > 0 && p->n_groups > 0) {
@@ -1034,7 +1046,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     void* targs[] = {&p->d_trp, &Sv, &Ni, &Tv, &p->d_spec_t0, &p->d_spec_K, &p->d_trsum};
     rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
     if (rc) return rc;
-    rc = launch(bwd, grid, block, eargs, p->smem_bytes, p->stream, p->multi);
+    rc = launch(bwd, grid, bblock, eargs, bsm, p->stream, p->multi);
     if (rc) return rc;
   }
   p->mark(3);
@@ -1056,6 +1068,55 @@ int check_field(lg_problem* p, long N, double dt, const double* amps) {
     for (long q = 0; q < N * p->Kc; ++q)
       if (!std::isfinite(amps[q])) return fail(LG_INVALID_ARG, "control amplitudes must be finite");
   return LG_OK;
+}
+
+// Warp-specialised engine (lg_sweep_ws.cu): small sparse problems, one CTA per trajectory.
+bool configure_ws(lg_problem* p, int smem_optin) {
+  if (p->dense || p->W > 9 || p->d > 128 || p->Wc > 2 || p->Kc > 7) return false;
+  int nspec[2] = {0, 0};
+  int Wp = 1;
+  for (auto& s : p->specs) {
+    nspec[s.set]++;
+    if (s.kind == LG_STATE_PENALTY) Wp = std::max(Wp, s.pen_W);
+  }
+  const int Imax = std::max(nspec[0], nspec[1]);
+  if (Imax > 4 || p->Kc + 1 + Imax > 8) return false;
+  std::vector<int> gset, gt0, gnT;
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    for (int a2 = lo; a2 < hi; ++a2) {
+      gset.push_back(s);
+      gt0.push_back(p->set_t0[s] + a2);
+      gnT.push_back(1);
+    }
+  }
+  if (gset.empty() || gset.size() > 64) return false;
+  const int rpl = p->d <= 64 ? 1 : 2;
+  const int fw = lg_ws_layout_words((int)p->d, 2, Imax, Wp), bw = lg_ws_layout_words((int)p->d, p->Kc + 1 + Imax, Imax, Wp);
+  if ((long)std::max(fw, bw) * 16 > std::min(smem_optin, 227 * 1024)) return false;
+  void* f0 = lg_ws_kernel(0, p->W, rpl);
+  void* f1 = lg_ws_kernel(1, p->W, rpl);
+  if (!f0 || !f1) return false;
+  if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, fw * 16) != cudaSuccess ||
+      cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, bw * 16) != cudaSuccess)
+    return false;
+  p->engine = 4;
+  p->multi = false;
+  p->ws_rpl = rpl;
+  p->ws_fwd_smem = fw * 16;
+  p->ws_bwd_smem = bw * 16;
+  p->ws_bwd_threads = (p->Kc + 1 + Imax) * 64;
+  p->threads = 128;
+  p->n_slabs = 1;
+  p->grp_set = gset;
+  p->grp_t0 = gt0;
+  p->grp_nT = gnT;
+  p->n_groups = (int)gset.size();
+  p->live_peak = 4 * (p->Kc + 1 + Imax) + 4 * (1 + Imax);
+  p->d_bar = p->mem.alloc<unsigned>(4 * (size_t)std::max(p->n_groups, 1));
+  p->d_scratch = p->mem.alloc<double2>(1);
+  p->d_red = p->mem.alloc<double2>(1);
+  return true;
 }
 
 // CTA engine: one CTA per trajectory (up to 64 groups), everything in shared memory.
@@ -1151,6 +1212,7 @@ int configure(lg_problem* p) {
   bool multi = d > 4096;
   if (fs == "multi") multi = true;
   if (fs == "single" || fs == "legacy") multi = false;
+  if (!multi && fs != "single" && fs != "legacy" && fs != "cta" && configure_ws(p, smem_optin)) return LG_OK;
   if (!multi && fs != "single" && fs != "legacy" && configure_cta(p, nsm, smem_optin)) return LG_OK;
   if (!g_err.empty() && g_err.rfind("cta:", 0) == 0) g_err.clear();
   int nsets = (p->set_T[0] > 0) + (p->set_T[1] > 0);
