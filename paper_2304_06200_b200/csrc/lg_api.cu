@@ -250,6 +250,7 @@ struct lg_problem {
   std::vector<double2*> d_hc_dense_host;
   int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
   int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
+  bool ws_cluster = false;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
   long scratch_per_group = 0;
   std::vector<int> grp_set, grp_t0, grp_nT;
@@ -573,6 +574,19 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.trp = p->d_trp;
   E.psiN = p->d_psiN;
   E.trsum = p->d_trsum;
+  E.trace = nullptr;
+  if (std::getenv("LG_TRACE") && p->engine == 4) {
+    static long long* tbuf = nullptr;
+    static size_t tcap = 0;
+    const size_t need = (size_t)p->n_groups * 8 * N * 4;
+    if (need > tcap) {
+      if (tbuf) cudaFree(tbuf);
+      cudaMalloc(&tbuf, need * sizeof(long long));
+      tcap = need;
+    }
+    cudaMemset(tbuf, 0, need * sizeof(long long));
+    E.trace = tbuf;
+  }
   return E;
 }
 
@@ -1046,8 +1060,35 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     void* targs[] = {&p->d_trp, &Sv, &Ni, &Tv, &p->d_spec_t0, &p->d_spec_K, &p->d_trsum};
     rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
     if (rc) return rc;
-    rc = launch(bwd, grid, bblock, eargs, bsm, p->stream, p->multi);
-    if (rc) return rc;
+    if (p->engine == 4 && p->ws_cluster) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(p->n_groups * (p->Kc + 1));
+      cfg.blockDim = bblock;
+      cfg.dynamicSmemBytes = bsm;
+      cfg.stream = p->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = p->Kc + 1;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelExC(&cfg, lg_ws_kernel(2, p->W, p->ws_rpl), eargs);
+      if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
+    } else {
+      rc = launch(bwd, grid, bblock, eargs, bsm, p->stream, p->multi);
+      if (rc) return rc;
+    }
+    if (E.trace) {
+      const size_t need = (size_t)p->n_groups * 8 * N * 4;
+      std::vector<long long> h(need);
+      cudaStreamSynchronize(p->stream);
+      cudaMemcpy(h.data(), E.trace, need * sizeof(long long), cudaMemcpyDeviceToHost);
+      if (FILE* f = std::fopen(std::getenv("LG_TRACE"), "wb")) {
+        std::fwrite(h.data(), sizeof(long long), need, f);
+        std::fclose(f);
+      }
+    }
   }
   p->mark(3);
   LgFinalArgs F = final_args(p, N, p->d_ip, p->d_fin, p->d_run, p->d_trp, p->d_grad, p->d_cost);
@@ -1072,7 +1113,7 @@ int check_field(lg_problem* p, long N, double dt, const double* amps) {
 
 // Warp-specialised engine (lg_sweep_ws.cu): small sparse problems, one CTA per trajectory.
 bool configure_ws(lg_problem* p, int smem_optin) {
-  if (p->dense || p->W > 9 || p->d > 128 || p->Wc > 2 || p->Kc > 7) return false;
+  if (p->dense || p->W > 9 || p->d > 64 || p->Wc > 2 || p->Kc > 6) return false;
   int nspec[2] = {0, 0};
   int Wp = 1;
   for (auto& s : p->specs) {
@@ -1097,6 +1138,17 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   void* f0 = lg_ws_kernel(0, p->W, rpl);
   void* f1 = lg_ws_kernel(1, p->W, rpl);
   if (!f0 || !f1) return false;
+  // cluster variant: one CTA per derivative team + one for psi/costates
+  const char* nc = std::getenv("LG_WS_NOCLUSTER");
+  const int cw = lg_ws_layout_words((int)p->d, 1 + Imax, Imax, Wp);
+  p->ws_cluster = !nc && p->Kc + 1 <= 8 && (long)cw * 16 <= std::min(smem_optin, 227 * 1024);
+  if (p->ws_cluster) {
+    void* f2 = lg_ws_kernel(2, p->W, rpl);
+    if (!f2 || cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, cw * 16) != cudaSuccess)
+      p->ws_cluster = false;
+    else
+      cudaFuncSetAttribute(f2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
   if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, fw * 16) != cudaSuccess ||
       cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, bw * 16) != cudaSuccess)
     return false;
@@ -1105,7 +1157,8 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   p->ws_rpl = rpl;
   p->ws_fwd_smem = fw * 16;
   p->ws_bwd_smem = bw * 16;
-  p->ws_bwd_threads = (p->Kc + 1 + Imax) * 64;
+  p->ws_bwd_threads = p->ws_cluster ? std::max(128, (1 + Imax) * 64) : (p->Kc + 1 + Imax) * 64;
+  if (p->ws_cluster) p->ws_bwd_smem = cw * 16;
   p->threads = 128;
   p->n_slabs = 1;
   p->grp_set = gset;

@@ -61,62 +61,162 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
       "r"(parity)
       : "memory");
 }
+// ---- cluster (DSMEM) helpers
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smaddr(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st(unsigned addr, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void cl_arrive(unsigned addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mb_wait_cl(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra "
+      "WAITC_%=;\n}\n" ::"r"(smaddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void team_sync(int id) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(TEAM) : "memory"); }
 
 struct Team {
   int id;    // named barrier id (1..15)
-  int tl;    // thread index within team [0, 64)
+  int tl;    // thread index within team
+  int tsz;   // 32 (single warp: __syncwarp) or 64 (two warps: named barrier)
   int d;
 };
 
+__device__ __forceinline__ void tsync(const Team& tm) {
+  if (tm.tsz == 32)
+    __syncwarp();
+  else
+    team_sync(tm.id);
+}
+
+// One Taylor term: Y <- (A X) r (+ cur when LAST), rows owned by this lane.
+// ox/oy: shared offsets of the two term buffers; addresses of the operand
+// slots are loop invariant (the caller alternates two fixed buffers).
+template <int W, int RPL, int NC>
+__device__ __forceinline__ void team_term(const Team& tm, double2 (&cur)[NC][RPL], const double2 (&a)[RPL][W],
+                                          const int (&col)[RPL][W], const double2 (&ac)[RPL][2],
+                                          const int (&accol)[RPL][2], int ox, int oy, double r, bool last) {
+  const int d = tm.d;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int i = tm.tl + k * tm.tsz;
+    if (i >= d) continue;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < W; ++w) cmac(p, q, a[k][w], ws_sm[ox + c * d + col[k][w]]);
+      if (NC == 2 && c == 0) {
+        cmac(p, q, ac[k][0], ws_sm[ox + d + accol[k][0]]);
+        cmac(p, q, ac[k][1], ws_sm[ox + d + accol[k][1]]);
+      }
+      const double2 tt = make_double2((p.x + q.x) * r, (p.y + q.y) * r);
+      cur[c][k] = cadd(cur[c][k], tt);
+      if (last)
+        ws_sm[oy + c * d + i] = cur[c][k];
+      else
+        ws_sm[oy + c * d + i] = tt;
+    }
+  }
+  tsync(tm);
+}
+
 // Per-team Taylor chain over NC columns (NC == 2: column 0 is the aux top with
-// the control generator acting on column 1, the bottom).  Input staged in tb0.
+// the control generator acting on column 1, the bottom).  Input staged in tb0;
+// the chain alternates tb0 -> tb1 -> tb0 ... two terms per loop trip.
 template <int W, int RPL, int NC>
 __device__ __forceinline__ void team_chain(const Team& tm, double2 (&cur)[NC][RPL], const double2 (&a)[RPL][W],
                                            const int (&col)[RPL][W], const double2 (&ac)[RPL][2],
                                            const int (&accol)[RPL][2], int m, int s, double sgn, int tb0, int tb1,
                                            int rt) {
-  const int d = tm.d;
   if (tm.tl < m) ws_sm[rt + tm.tl].x = sgn * (1.0 / (double)(s * (tm.tl + 1)));
-  team_sync(tm.id);
-  int X = tb0, Y = tb1;
-  for (int si = 0; si < s; ++si) {
-    for (int j = 1; j <= m; ++j) {
-      const double r = ws_sm[rt + j - 1].x;
-      const bool last = j == m;
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        if (i >= d) continue;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int xc = X + c * d;
-          double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
-#pragma unroll
-          for (int w = 0; w < W; ++w) cmac(p, q, a[k][w], ws_sm[xc + col[k][w]]);
-          if (NC == 2 && c == 0) {
-            cmac(p, q, ac[k][0], ws_sm[X + d + accol[k][0]]);
-            cmac(p, q, ac[k][1], ws_sm[X + d + accol[k][1]]);
-          }
-          const double2 tt = make_double2((p.x + q.x) * r, (p.y + q.y) * r);
-          cur[c][k] = cadd(cur[c][k], tt);
-          ws_sm[Y + c * d + i] = last ? cur[c][k] : tt;
-        }
-      }
-      team_sync(tm.id);
-      const int t_ = X;
-      X = Y;
-      Y = t_;
+  tsync(tm);
+  const int total = m * s;
+  int j = 1;  // position within the current scaling round
+  for (int t = 0; t < total; t += 2) {
+    team_term<W, RPL, NC>(tm, cur, a, col, ac, accol, tb0, tb1, ws_sm[rt + j - 1].x, j == m);
+    j = j == m ? 1 : j + 1;
+    if (t + 1 == total) {
+      // odd number of terms: result is in tb1; callers only use cur registers
+      break;
     }
+    team_term<W, RPL, NC>(tm, cur, a, col, ac, accol, tb1, tb0, ws_sm[rt + j - 1].x, j == m);
+    j = j == m ? 1 : j + 1;
+  }
+}
+
+// Derivative team of four warps: warps 0-1 own the aux top column, warps 2-3
+// the bottom column, one row per lane.  Per term every thread first loads all
+// its operand slots, then accumulates, then stores (no store->load ordering
+// between the two columns), and the team meets at a 128-thread named barrier.
+template <int W>
+__device__ __forceinline__ void x4_chain(int bar_id, int i, int d, bool top, double2& cur, const double2 (&a)[W],
+                                         const int (&col)[W], const double2 (&ac)[2], const int (&accol)[2], int m,
+                                         int s, int tb0, int tb1, int rt, int tl) {
+  if (tl < m) ws_sm[rt + tl].x = 1.0 / (double)(s * (tl + 1));
+  asm volatile("bar.sync %0, 128;\n" ::"r"(bar_id) : "memory");
+  const int total = m * s;
+  const int c = top ? 0 : d;  // own column offset inside a term buffer
+  int X = tb0, Y = tb1, j = 1;
+  for (int t = 0; t < total; ++t) {
+    const double r = ws_sm[rt + j - 1].x;
+    const bool last = j == m;
+    if (i < d) {
+      double2 x[W], y[2];
+#pragma unroll
+      for (int w = 0; w < W; ++w) x[w] = ws_sm[X + c + col[w]];
+      if (top) {
+        y[0] = ws_sm[X + d + accol[0]];
+        y[1] = ws_sm[X + d + accol[1]];
+      }
+      double2 p0 = make_double2(0.0, 0.0), q0 = make_double2(0.0, 0.0);
+      double2 p1 = make_double2(0.0, 0.0), q1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (w & 1)
+          cmac(p1, q1, a[w], x[w]);
+        else
+          cmac(p0, q0, a[w], x[w]);
+      }
+      if (top) {
+        cmac(p1, q1, ac[0], y[0]);
+        cmac(p0, q0, ac[1], y[1]);
+      }
+      const double2 tt = make_double2(((p0.x + q0.x) + (p1.x + q1.x)) * r, ((p0.y + q0.y) + (p1.y + q1.y)) * r);
+      cur = cadd(cur, tt);
+      ws_sm[Y + c + i] = last ? cur : tt;
+    }
+    asm volatile("bar.sync %0, 128;\n" ::"r"(bar_id) : "memory");
+    const int t_ = X;
+    X = Y;
+    Y = t_;
+    j = last ? 1 : j + 1;
   }
 }
 
 template <int W, int RPL>
-__device__ __forceinline__ void load_rows(const LgEngineArgs& E, int n, int tl, double2 (&a)[RPL][W], int (&col)[RPL][W]) {
+__device__ __forceinline__ void load_rows(const LgEngineArgs& E, int n, int tl, int tsz, double2 (&a)[RPL][W],
+                                          int (&col)[RPL][W]) {
   const double2* src = E.A + (long)n * W * E.d;
 #pragma unroll
   for (int k = 0; k < RPL; ++k) {
-    const int i = tl + k * TEAM;
+    const int i = tl + k * tsz;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const bool ok = i < E.d;
@@ -126,18 +226,23 @@ __device__ __forceinline__ void load_rows(const LgEngineArgs& E, int n, int tl, 
   }
 }
 
-// Team-wide deterministic sum of NV complex values (thread partials) -> res[0..NV) for all team threads.
+// Team-wide deterministic sum of nv (<= NV) complex values -> v[0..nv) for all team threads.
 template <int NV>
-__device__ __forceinline__ void team_reduce(const Team& tm, double2 (&v)[NV], int red) {
+__device__ __forceinline__ void team_reduce(const Team& tm, double2 (&v)[NV], int nv, int red) {
   const int w = tm.tl >> 5, l = tm.tl & 31;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
+    if (q >= nv) break;
     v[q] = warp_sum(v[q]);
-    if (l == 0) ws_sm[red + q * 2 + w] = v[q];
+    if (tm.tsz == 64 && l == 0) ws_sm[red + q * 2 + w] = v[q];
   }
+  if (tm.tsz == 32) return;
   team_sync(tm.id);
 #pragma unroll
-  for (int q = 0; q < NV; ++q) v[q] = cadd(ws_sm[red + q * 2], ws_sm[red + q * 2 + 1]);
+  for (int q = 0; q < NV; ++q) {
+    if (q >= nv) break;
+    v[q] = cadd(ws_sm[red + q * 2], ws_sm[red + q * 2 + 1]);
+  }
   team_sync(tm.id);
 }
 
@@ -190,23 +295,10 @@ __device__ __forceinline__ double2 pen_row(int d, int Wp, int pen, const int* pc
 
 extern "C" __global__ void lg_ws_dummy() {}
 
-// ------------------------------------------------------------------------------------------ forward
-// teams: 0 = propagation P, 1 = scalars F.   blockDim = 2 * TEAM.
-template <int W, int RPL>
-__global__ void __launch_bounds__(2 * TEAM, 1) lg_k_ws_forward(const __grid_constant__ LgEngineArgs E) {
-  const int d = E.d, g = blockIdx.x;
-  const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
-  const int I = E.set_nspec[set];
-  int Wp = 1;
-  for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
-  const WsLay L = ws_layout(d, 2, I, Wp);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
-  unsigned long long* full = bars;
-  unsigned long long* empty = bars + RING;
-  int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
-  const int team = threadIdx.x / TEAM;
-  Team tm{team + 1, (int)threadIdx.x % TEAM, d};
-  // stage targets / penalty operators
+// Stage the targets / penalty operators of this set into shared memory.
+__device__ __forceinline__ void stage_specs(const LgEngineArgs& E, const WsLay& L, int set, int trel, int I, int Wp,
+                                            int* pcol) {
+  const int d = E.d;
   for (int si = 0; si < I; ++si) {
     const LgSpecDev& sp = E.spec[E.set_spec[set][si]];
     for (int i = threadIdx.x; i < d; i += blockDim.x)
@@ -218,100 +310,93 @@ __global__ void __launch_bounds__(2 * TEAM, 1) lg_k_ws_forward(const __grid_cons
       pcol[si * Wp * d + q] = ok ? sp.pen_cols[q] : (q % d);
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------ forward
+// warps 0-1: propagation team P; warps 2-3: per-step scalars team F.  d <= 64.
+template <int W>
+__global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant__ LgEngineArgs E) {
+  const int d = E.d, g = blockIdx.x, N = E.N;
+  const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
+  const int I = E.set_nspec[set];
+  int Wp = 1;
+  for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
+  const WsLay L = ws_layout(d, 2, I, Wp);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
+  unsigned long long* full = bars;
+  unsigned long long* empty = bars + RING;
+  int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
+  const int team = threadIdx.x / 64;
+  const Team tm{team + 1, (int)threadIdx.x % 64, 64, d};
+  stage_specs(E, L, set, trel, I, Wp, pcol);
   if (threadIdx.x == 0) {
     for (int j = 0; j < RING; ++j) {
-      mb_init(&full[j], TEAM);
+      mb_init(&full[j], 64);
       mb_init(&empty[j], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int N = E.N;
   const int tb0 = L.tb + team * 4 * d, tb1 = tb0 + 2 * d;
+  const int i = tm.tl;
   if (team == 0) {
     // ---------------- P: forward propagation
-    double2 cur[1][RPL];
-    double2 a[RPL][W], an[RPL][W];
-    int col[RPL][W], coln[RPL][W];
-    double2 ac[RPL][2];
-    int accol[RPL][2];
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) ac[k][0] = ac[k][1] = make_double2(0.0, 0.0), accol[k][0] = accol[k][1] = 0;
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
-      if (i < d) ws_sm[tb0 + i] = E.psi0[(long)t0 * d + i];
-    }
-    load_rows<W, RPL>(E, 0, tm.tl, an, coln);
+    double2 cur[1][1];
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    const double2 ac[1][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
+    const int accol[1][2] = {{0, 0}};
+    if (i < d) ws_sm[tb0 + i] = E.psi0[(long)t0 * d + i];
+    load_rows<W, 1>(E, 0, tm.tl, 64, an, coln);
     int4 pln = E.plan[0];
-    team_sync(tm.id);
     for (int n = 0; n < N; ++n) {
       const int4 pl = pln;
 #pragma unroll
-      for (int k = 0; k < RPL; ++k)
-#pragma unroll
-        for (int w = 0; w < W; ++w) a[k][w] = an[k][w], col[k][w] = coln[k][w];
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
       if (n + 1 < N) {
-        load_rows<W, RPL>(E, n + 1, tm.tl, an, coln);
+        load_rows<W, 1>(E, n + 1, tm.tl, 64, an, coln);
         pln = E.plan[(long)(n + 1) * (E.Kc + 1)];
       }
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        cur[0][k] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
-      }
-      team_chain<W, RPL, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+      cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
+      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
       const int slot = n % RING, use = n / RING;
       if (use > 0) mb_wait(&empty[slot], (use - 1) & 1);
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        if (i < d) {
-          ws_sm[L.ring + slot * d + i] = cur[0][k];
-          ws_sm[tb0 + i] = cur[0][k];
-        }
+      if (i < d) {
+        ws_sm[L.ring + slot * d + i] = cur[0][0];
+        ws_sm[tb0 + i] = cur[0][0];
       }
       mb_arrive(&full[slot]);
       team_sync(tm.id);
     }
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
-      if (i < d) E.psiN[(long)t0 * d + i] = cur[0][k];
-    }
+    if (i < d) E.psiN[(long)t0 * d + i] = cur[0][0];
   } else {
     // ---------------- F: per-step scalars from the psi ring
-    double runacc[LG_MAX_SPECS];
-    for (int si = 0; si < LG_MAX_SPECS; ++si) runacc[si] = 0.0;
+    double runacc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int n = 0; n < N; ++n) {
       const int slot = n % RING, use = n / RING;
       mb_wait(&full[slot], use & 1);
       const int psi = L.ring + slot * d;
-      const bool fin = n == N - 1;
       double2 v[4];
 #pragma unroll
-      for (int si = 0; si < 4; ++si) v[si] = make_double2(0.0, 0.0);
-      for (int si = 0; si < I; ++si) {
-        const int kind = E.spec[E.set_spec[set][si]].kind;
-        for (int k = 0; k < RPL; ++k) {
-          const int i = tm.tl + k * TEAM;
-          if (i >= d) continue;
-          const double2 pv = ws_sm[psi + i];
+      for (int q = 0; q < 4; ++q) v[q] = make_double2(0.0, 0.0);
+      if (i < d) {
+        const double2 pv = ws_sm[psi + i];
+        for (int si = 0; si < I; ++si) {
+          const int kind = E.spec[E.set_spec[set][si]].kind;
           if (kind == LGK_STATE_PEN)
-            v[si] = cadd(v[si], cdot(pv, pen_row(d, Wp, L.pen + si * Wp * d, pcol + si * Wp * d, i, psi)));
+            v[si] = cdot(pv, pen_row(d, Wp, L.pen + si * Wp * d, pcol + si * Wp * d, i, psi));
           else if (kind == LGK_STATE_INF)
-            v[si] = cadd(v[si], cdot(pv, ws_sm[L.tgt + si * d + i]));
+            v[si] = cdot(pv, ws_sm[L.tgt + si * d + i]);
           else
-            v[si] = cadd(v[si], cdot(ws_sm[L.tgt + si * d + i], pv));
+            v[si] = cdot(ws_sm[L.tgt + si * d + i], pv);
         }
       }
-      team_reduce<4>(tm, v, L.red + team * 2 * LG_MAX_SPECS);
+      team_reduce<4>(tm, v, I, L.red + team * 2 * LG_MAX_SPECS);
       if (tm.tl == 0) {
         mb_arrive(&empty[slot]);
         for (int si = 0; si < I; ++si) {
           const int sidx = E.set_spec[set][si];
           const int kind = E.spec[sidx].kind;
-          const long o = (long)sidx * E.T_total + t0;
           if (kind == LGK_STATE_PEN) {
             runacc[si] += v[si].x;
           } else if (kind == LGK_STATE_RUN) {
@@ -319,8 +404,8 @@ __global__ void __launch_bounds__(2 * TEAM, 1) lg_k_ws_forward(const __grid_cons
             runacc[si] += h * h;
           } else if (kind == LGK_GATE_RUN) {
             E.trp[((long)sidx * N + n) * E.T_total + t0] = v[si];
-          } else if (fin) {
-            E.fin[o] = v[si];
+          } else if (n == N - 1) {
+            E.fin[(long)sidx * E.T_total + t0] = v[si];
           }
         }
       }
@@ -335,9 +420,9 @@ __global__ void __launch_bounds__(2 * TEAM, 1) lg_k_ws_forward(const __grid_cons
 }
 
 // ------------------------------------------------------------------------------------------ backward
-// teams: X_0..X_{Kc-1}, P, L_0..L_{I-1}.   blockDim = (Kc + 1 + I) * TEAM.
-template <int W, int RPL>
-__global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_constant__ LgEngineArgs E) {
+// teams of two warps (one row per lane): X_0..X_{Kc-1}, P, L_0..L_{I-1}.  d <= 64.
+template <int W>
+__global__ void __launch_bounds__(512, 1) lg_k_ws_backward(const __grid_constant__ LgEngineArgs E) {
   const int d = E.d, g = blockIdx.x, Kc = E.Kc, N = E.N;
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set];
@@ -346,38 +431,26 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
   const int nteams = Kc + 1 + I;
   const WsLay L = ws_layout(d, nteams, I, Wp);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
-  unsigned long long* pfull = bars;                // [RING]
-  unsigned long long* pempty = bars + RING;        // [RING]
-  unsigned long long* lfull = bars + 2 * RING;     // [I][RING]
-  unsigned long long* lempty = lfull + I * RING;   // [I][RING]
+  unsigned long long* pfull = bars;               // [RING]
+  unsigned long long* pempty = bars + RING;       // [RING]
+  unsigned long long* lfull = bars + 2 * RING;    // [I][RING]
+  unsigned long long* lempty = lfull + I * RING;  // [I][RING]
   int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
-  const int team = threadIdx.x / TEAM;
-  Team tm{team + 1, (int)threadIdx.x % TEAM, d};
-  const int Xteams = Kc, Pteam = Kc;
-  // psi consumers: all X teams + L teams whose source needs psi_{n-1}
+  const int team = threadIdx.x >> 6, tl = threadIdx.x & 63;
+  const Team tm{team + 1, tl, 64, d};
   int n_lpsi = 0;
   for (int si = 0; si < I; ++si) {
     const int kind = E.spec[E.set_spec[set][si]].kind;
     n_lpsi += (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN);
   }
-  for (int si = 0; si < I; ++si) {
-    const LgSpecDev& sp = E.spec[E.set_spec[set][si]];
-    for (int i = threadIdx.x; i < d; i += blockDim.x)
-      ws_sm[L.tgt + si * d + i] = sp.tgt ? sp.tgt[(long)trel * d + i] : make_double2(0.0, 0.0);
-    for (int q = threadIdx.x; q < Wp * d; q += blockDim.x) {
-      const int w = q / d;
-      const bool ok = sp.kind == LGK_STATE_PEN && w < sp.pen_W;
-      ws_sm[L.pen + si * Wp * d + q] = ok ? sp.pen_vals[q] : make_double2(0.0, 0.0);
-      pcol[si * Wp * d + q] = ok ? sp.pen_cols[q] : (q % d);
-    }
-  }
+  stage_specs(E, L, set, trel, I, Wp, pcol);
   if (threadIdx.x == 0) {
     for (int j = 0; j < RING; ++j) {
-      mb_init(&pfull[j], TEAM);
-      mb_init(&pempty[j], Xteams + n_lpsi);
+      mb_init(&pfull[j], 64);
+      mb_init(&pempty[j], Kc + n_lpsi);
       for (int si = 0; si < I; ++si) {
-        mb_init(&lfull[si * RING + j], TEAM);
-        mb_init(&lempty[si * RING + j], Xteams);
+        mb_init(&lfull[si * RING + j], 64);
+        mb_init(&lempty[si * RING + j], Kc);
       }
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -386,70 +459,58 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
   if (team >= nteams) return;  // set with fewer cost terms than the widest set
   const int tb0 = L.tb + team * 4 * d, tb1 = tb0 + 2 * d, rt = L.rt + team * 64;
   const int red = L.red + team * 2 * LG_MAX_SPECS;
-  double2 a[RPL][W], an[RPL][W];
-  int col[RPL][W], coln[RPL][W];
-  double2 ac[RPL][2];
-  int accol[RPL][2];
-#pragma unroll
-  for (int k = 0; k < RPL; ++k) ac[k][0] = ac[k][1] = make_double2(0.0, 0.0), accol[k][0] = accol[k][1] = 0;
-  load_rows<W, RPL>(E, N - 1, tm.tl, an, coln);
 
-  if (team < Xteams) {
-    // ---------------- X_k: derivative products and inner products
-    const int kch = team;
+  if (team < Kc) {
+    // ---------------- X_k: derivative products and inner products (one row per lane)
+    const int kch = team, i = tl;
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    double2 ac[1][2];
+    int accol[1][2];
 #pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
-#pragma unroll
-      for (int w = 0; w < 2; ++w) {
-        const bool ok = i < d && w < E.Wc;
-        ac[k][w] = ok ? E.Ac[((long)kch * E.Wc + w) * d + i] : make_double2(0.0, 0.0);
-        accol[k][w] = ok ? E.Ac_cols[((long)kch * E.Wc + w) * d + i] : 0;
-      }
+    for (int w = 0; w < 2; ++w) {
+      const bool ok = i < d && w < E.Wc;
+      ac[0][w] = ok ? E.Ac[((long)kch * E.Wc + w) * d + i] : make_double2(0.0, 0.0);
+      accol[0][w] = ok ? E.Ac_cols[((long)kch * E.Wc + w) * d + i] : 0;
     }
+    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1) + 1 + kch];
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int4 pl = pln;
 #pragma unroll
-      for (int k = 0; k < RPL; ++k)
-#pragma unroll
-        for (int w = 0; w < W; ++w) a[k][w] = an[k][w], col[k][w] = coln[k][w];
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
       if (n > 0) {
-        load_rows<W, RPL>(E, n - 1, tm.tl, an, coln);
+        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
         pln = E.plan[(long)(n - 1) * (Kc + 1) + 1 + kch];
       }
       const int slot = it % RING, use = it / RING;
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + team) * N + it) * 4 : nullptr;
+      if (trc && tl == 0) trc[0] = clock64();
       mb_wait(&pfull[slot], use & 1);
-      double2 cur[2][RPL];
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        const double2 v = i < d ? ws_sm[L.ring + slot * d + i] : make_double2(0.0, 0.0);
-        cur[0][k] = make_double2(0.0, 0.0);
-        cur[1][k] = v;
-        if (i < d) {
-          ws_sm[tb0 + i] = make_double2(0.0, 0.0);
-          ws_sm[tb0 + d + i] = v;
-        }
+      if (trc && tl == 0) trc[1] = clock64();
+      double2 cur[2][1];
+      const double2 v0 = i < d ? ws_sm[L.ring + slot * d + i] : make_double2(0.0, 0.0);
+      cur[0][0] = make_double2(0.0, 0.0);
+      cur[1][0] = v0;
+      if (i < d) {
+        ws_sm[tb0 + i] = make_double2(0.0, 0.0);
+        ws_sm[tb0 + d + i] = v0;
       }
       team_sync(tm.id);
-      if (tm.tl == 0) mb_arrive(&pempty[slot]);
-      team_chain<W, RPL, 2>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, rt);
-      // inner products with lambda_s(n)
+      if (tl == 0) mb_arrive(&pempty[slot]);
+      team_chain<W, 1, 2>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, rt);
+      if (trc && tl == 0) trc[2] = clock64();
       double2 v[4];
 #pragma unroll
-      for (int si = 0; si < 4; ++si) v[si] = make_double2(0.0, 0.0);
+      for (int q = 0; q < 4; ++q) v[q] = make_double2(0.0, 0.0);
       for (int si = 0; si < I; ++si) {
         mb_wait(&lfull[si * RING + slot], use & 1);
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-          const int i = tm.tl + k * TEAM;
-          if (i < d) v[si] = cadd(v[si], cdot(ws_sm[L.lring + (si * RING + slot) * d + i], cur[0][k]));
-        }
+        if (i < d) v[si] = cdot(ws_sm[L.lring + (si * RING + slot) * d + i], cur[0][0]);
       }
-      team_reduce<4>(tm, v, red);
-      if (tm.tl == 0) {
+      team_reduce<4>(tm, v, I, red);
+      if (trc && tl == 0) trc[3] = clock64();
+      if (tl == 0) {
         for (int si = 0; si < I; ++si) {
           mb_arrive(&lempty[si * RING + slot]);
           const int sidx = E.set_spec[set][si];
@@ -457,48 +518,44 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
         }
       }
     }
-  } else if (team == Pteam) {
+  } else if (team == Kc) {
     // ---------------- P: psi recovery by adjoint propagation
-    double2 cur[1][RPL];
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
-      if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
-    }
+    const int i = tl;
+    double2 cur[1][1];
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    const double2 ac[1][2] = {};
+    const int accol[1][2] = {};
+    if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
+    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     team_sync(tm.id);
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int4 pl = pln;
 #pragma unroll
-      for (int k = 0; k < RPL; ++k)
-#pragma unroll
-        for (int w = 0; w < W; ++w) a[k][w] = an[k][w], col[k][w] = coln[k][w];
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
       if (n > 0) {
-        load_rows<W, RPL>(E, n - 1, tm.tl, an, coln);
+        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
         pln = E.plan[(long)(n - 1) * (Kc + 1)];
       }
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        cur[0][k] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
-      }
-      team_chain<W, RPL, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + team) * N + it) * 4 : nullptr;
+      if (trc && tl == 0) trc[0] = clock64();
+      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (trc && tl == 0) trc[1] = clock64();
       const int slot = it % RING, use = it / RING;
       if (use > 0) mb_wait(&pempty[slot], (use - 1) & 1);
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
-        if (i < d) {
-          ws_sm[L.ring + slot * d + i] = cur[0][k];
-          ws_sm[tb0 + i] = cur[0][k];
-        }
+      if (trc && tl == 0) trc[2] = clock64();
+      if (i < d) {
+        ws_sm[L.ring + slot * d + i] = cur[0][0];
+        ws_sm[tb0 + i] = cur[0][0];
       }
       mb_arrive(&pfull[slot]);
       team_sync(tm.id);
     }
   } else {
-    // ---------------- L_s: costate chain + sources
+    // ---------------- L_s: costate chain + sources 
     const int si = team - Kc - 1;
     const int sidx = E.set_spec[set][si];
     const int kind = E.spec[sidx].kind;
@@ -506,27 +563,31 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
     const int tg = L.tgt + si * d;
     const int pen = L.pen + si * Wp * d;
     const int* pc = pcol + si * Wp * d;
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    const double2 ac[1][2] = {};
+    const int accol[1][2] = {};
     // costate initialisation from psi_N (src/costs.py:312-321, :457-460); psi_N staged in tb1
 #pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
+    for (int k = 0; k < 1; ++k) {
+      const int i = tl;
       if (i < d) ws_sm[tb1 + i] = E.psiN[(long)t0 * d + i];
     }
     team_sync(tm.id);
     double2 ov[1] = {make_double2(0.0, 0.0)};
     if (kind == LGK_STATE_RUN) {
 #pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
+      for (int k = 0; k < 1; ++k) {
+        const int i = tl;
         if (i < d) ov[0] = cadd(ov[0], cdot(ws_sm[tg + i], ws_sm[tb1 + i]));
       }
-      team_reduce<1>(tm, ov, red);
+      team_reduce<1>(tm, ov, 1, red);
     }
     const double2 trN = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + N - 1] : make_double2(0.0, 0.0);
-    double2 cur[1][RPL];
+    double2 cur[1][1];
 #pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int i = tm.tl + k * TEAM;
+    for (int k = 0; k < 1; ++k) {
+      const int i = tl;
       double2 v = make_double2(0.0, 0.0);
       if (i < d) {
         if (kind == LGK_STATE_PEN)
@@ -541,15 +602,19 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
       cur[0][k] = v;
     }
     team_sync(tm.id);
+    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int slot = it % RING, use = it / RING;
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + team) * N + it) * 4 : nullptr;
+      if (trc && tl == 0) trc[0] = clock64();
       // publish lambda_s(n) for the X teams; it is also the chain input
       if (use > 0) mb_wait(&lempty[si * RING + slot], (use - 1) & 1);
+      if (trc && tl == 0) trc[1] = clock64();
 #pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = tm.tl + k * TEAM;
+      for (int k = 0; k < 1; ++k) {
+        const int i = tl;
         if (i < d) {
           ws_sm[L.lring + (si * RING + slot) * d + i] = cur[0][k];
           ws_sm[tb0 + i] = cur[0][k];
@@ -559,45 +624,43 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
       if (n == 0) break;
       const int4 pl = pln;
 #pragma unroll
-      for (int k = 0; k < RPL; ++k)
-#pragma unroll
-        for (int w = 0; w < W; ++w) a[k][w] = an[k][w], col[k][w] = coln[k][w];
-      if (n > 0) {
-        load_rows<W, RPL>(E, n - 1, tm.tl, an, coln);
-        pln = E.plan[(long)(n - 1) * (Kc + 1)];
-      }
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+      load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+      pln = E.plan[(long)(n - 1) * (Kc + 1)];
       const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
       team_sync(tm.id);
-      team_chain<W, RPL, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (trc && tl == 0) trc[2] = clock64();
       if (needs_psi) {
         mb_wait(&pfull[slot], use & 1);
+        if (trc && tl == 0) trc[3] = clock64();
         const int psi = L.ring + slot * d;
         if (kind == LGK_STATE_RUN) {
           double2 o2[1] = {make_double2(0.0, 0.0)};
 #pragma unroll
-          for (int k = 0; k < RPL; ++k) {
-            const int i = tm.tl + k * TEAM;
+          for (int k = 0; k < 1; ++k) {
+            const int i = tl;
             if (i < d) o2[0] = cadd(o2[0], cdot(ws_sm[tg + i], ws_sm[psi + i]));
           }
-          team_reduce<1>(tm, o2, red);
+          team_reduce<1>(tm, o2, 1, red);
 #pragma unroll
-          for (int k = 0; k < RPL; ++k) {
-            const int i = tm.tl + k * TEAM;
+          for (int k = 0; k < 1; ++k) {
+            const int i = tl;
             if (i < d) cur[0][k] = cadd(cur[0][k], cmul(ws_sm[tg + i], o2[0]));
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < RPL; ++k) {
-            const int i = tm.tl + k * TEAM;
+          for (int k = 0; k < 1; ++k) {
+            const int i = tl;
             if (i < d) cur[0][k] = cadd(cur[0][k], pen_row(d, Wp, pen, pc, i, psi));
           }
-          team_sync(tm.id);
         }
-        if (tm.tl == 0) mb_arrive(&pempty[slot]);
+        team_sync(tm.id);
+        if (tl == 0) mb_arrive(&pempty[slot]);
       } else if (kind == LGK_GATE_RUN) {
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-          const int i = tm.tl + k * TEAM;
+        for (int k = 0; k < 1; ++k) {
+          const int i = tl;
           if (i < d) cur[0][k] = cadd(cur[0][k], cmul(ws_sm[tg + i], tr));
         }
       }
@@ -605,13 +668,256 @@ __global__ void __launch_bounds__(8 * TEAM, 1) lg_k_ws_backward(const __grid_con
   }
 }
 
+// ------------------------------------------------------------------------------------------ backward (cluster)
+// Cluster of 1 + Kc CTAs per trajectory.  Rank 0: psi team P and costate teams
+// L_s (two warps each); rank 1 + k: derivative team X_k alone on its SM.  P and
+// L_s push psi_{n-1} / lambda_s(n) rows into every X CTA's ring over DSMEM and
+// arrive remotely on that CTA's full barrier; X CTAs arrive remotely on rank 0's
+// empty barriers.  All waits acquire at cluster scope.
+template <int W>
+__global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constant__ LgEngineArgs E) {
+  const int d = E.d, Kc = E.Kc, N = E.N;
+  const unsigned rank = cl_rank();
+  const int g = blockIdx.x / (Kc + 1);
+  const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
+  const int I = E.set_nspec[set];
+  int Wp = 1;
+  for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
+  const WsLay L = ws_layout(d, 1 + I, I, Wp);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
+  unsigned long long* pfull = bars;               // [RING]  (every rank)
+  unsigned long long* pempty = bars + RING;       // [RING]  (rank 0)
+  unsigned long long* lfull = bars + 2 * RING;    // [I][RING] (X ranks)
+  unsigned long long* lempty = lfull + I * RING;  // [I][RING] (rank 0)
+  int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
+  const int team = threadIdx.x >> 6, tl = threadIdx.x & 63;
+  const Team tm{team + 1, tl, 64, d};
+  int n_lpsi = 0;
+  for (int si = 0; si < I; ++si) {
+    const int kind = E.spec[E.set_spec[set][si]].kind;
+    n_lpsi += (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN);
+  }
+  stage_specs(E, L, set, trel, I, Wp, pcol);
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < RING; ++j) {
+      mb_init(&pfull[j], 64);
+      mb_init(&pempty[j], Kc + n_lpsi);
+      for (int si = 0; si < I; ++si) {
+        mb_init(&lfull[si * RING + j], 64);
+        mb_init(&lempty[si * RING + j], Kc);
+      }
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  cl_sync();
+  const int i = tl;
+  const int tb0 = L.tb + team * 4 * d, tb1 = tb0 + 2 * d, rt = L.rt + team * 64;
+  const int red = L.red + team * 2 * LG_MAX_SPECS;
+  if (rank > 0 && threadIdx.x < 128) {
+    // ---------------- X_k on its own SM: four warps (top column | bottom column)
+    const int kch = rank - 1;
+    const int t4 = threadIdx.x;
+    const bool top = t4 < 64;
+    const int ix = t4 & 63;
+    double2 a[W], an[W];
+    int col[W], coln[W];
+    double2 ac[2];
+    int accol[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const bool ok = top && ix < d && w < E.Wc;
+      ac[w] = ok ? E.Ac[((long)kch * E.Wc + w) * d + ix] : make_double2(0.0, 0.0);
+      accol[w] = ok ? E.Ac_cols[((long)kch * E.Wc + w) * d + ix] : 0;
+    }
+    auto rows = [&](int n, double2 (&aa)[W], int (&cc)[W]) {
+      const double2* src = E.A + (long)n * W * d;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        aa[w] = ix < d ? src[(long)w * d + ix] : make_double2(0.0, 0.0);
+        cc[w] = ix < d ? E.A_cols[w * d + ix] : 0;
+      }
+    };
+    rows(N - 1, an, coln);
+    int4 pln = E.plan[(long)(N - 1) * (Kc + 1) + 1 + kch];
+    const int xb0 = L.tb, xb1 = L.tb + 2 * d, xrt = L.rt, xred = L.red;
+    for (int it = 0; it < N; ++it) {
+      const int n = N - 1 - it;
+      const int4 pl = pln;
+#pragma unroll
+      for (int w = 0; w < W; ++w) a[w] = an[w], col[w] = coln[w];
+      if (n > 0) {
+        rows(n - 1, an, coln);
+        pln = E.plan[(long)(n - 1) * (Kc + 1) + 1 + kch];
+      }
+      const int slot = it % RING, use = it / RING;
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + kch) * N + it) * 4 : nullptr;
+      if (trc && t4 == 0) trc[0] = clock64();
+      mb_wait_cl(&pfull[slot], use & 1);
+      if (trc && t4 == 0) trc[1] = clock64();
+      double2 cur = make_double2(0.0, 0.0);
+      if (ix < d) {
+        const double2 v0 = ws_sm[L.ring + slot * d + ix];
+        if (!top) cur = v0;
+        ws_sm[xb0 + (top ? 0 : d) + ix] = top ? make_double2(0.0, 0.0) : v0;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (t4 == 0) cl_arrive(cl_map(&pempty[slot], 0));
+      x4_chain<W>(1, ix, d, top, cur, a, col, ac, accol, pl.x, pl.y, xb0, xb1, xrt, t4);
+      if (trc && t4 == 0) trc[2] = clock64();
+      // <lambda_s(n) | D_k>: top threads hold D
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = make_double2(0.0, 0.0);
+      for (int si = 0; si < I; ++si) {
+        mb_wait_cl(&lfull[si * RING + slot], use & 1);
+        if (top && ix < d) v[si] = cdot(ws_sm[L.lring + (si * RING + slot) * d + ix], cur);
+      }
+      const int wq = t4 >> 5;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q >= I) break;
+        v[q] = warp_sum(v[q]);
+        if ((t4 & 31) == 0) ws_sm[xred + q * 4 + wq] = v[q];
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (trc && t4 == 0) trc[3] = clock64();
+      if (t4 == 0) {
+        for (int si = 0; si < I; ++si) {
+          const double2 r0 = cadd(cadd(ws_sm[xred + si * 4 + 0], ws_sm[xred + si * 4 + 1]),
+                                  cadd(ws_sm[xred + si * 4 + 2], ws_sm[xred + si * 4 + 3]));
+          cl_arrive(cl_map(&lempty[si * RING + slot], 0));
+          const int sidx = E.set_spec[set][si];
+          E.ip[(((long)n * E.n_specs + sidx) * Kc + kch) * E.T_total + t0] = r0;
+        }
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    }
+  } else if (rank == 0 && team == 0) {
+    // ---------------- P: psi recovery; pushes psi_{n-1} to every X CTA
+    double2 cur[1][1];
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    const double2 ac[1][2] = {};
+    const int accol[1][2] = {};
+    if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
+    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+    int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
+    team_sync(tm.id);
+    for (int it = 0; it < N; ++it) {
+      const int n = N - 1 - it;
+      const int4 pl = pln;
+#pragma unroll
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+      if (n > 0) {
+        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+        pln = E.plan[(long)(n - 1) * (Kc + 1)];
+      }
+      cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + Kc) * N + it) * 4 : nullptr;
+      if (trc && tl == 0) trc[0] = clock64();
+      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (trc && tl == 0) trc[1] = clock64();
+      const int slot = it % RING, use = it / RING;
+      if (use > 0) mb_wait_cl(&pempty[slot], (use - 1) & 1);
+      if (trc && tl == 0) trc[2] = clock64();
+      if (i < d) {
+        ws_sm[L.ring + slot * d + i] = cur[0][0];
+        ws_sm[tb0 + i] = cur[0][0];
+        for (int r = 1; r <= Kc; ++r) cl_st(cl_map(&ws_sm[L.ring + slot * d + i], r), cur[0][0]);
+      }
+      mb_arrive(&pfull[slot]);
+      for (int r = 1; r <= Kc; ++r) cl_arrive(cl_map(&pfull[slot], r));
+      team_sync(tm.id);
+    }
+  } else if (rank == 0 && team <= I) {
+    // ---------------- L_s: costate chain + sources; pushes lambda_s(n) to every X CTA
+    const int si = team - 1;
+    const int sidx = E.set_spec[set][si];
+    const int kind = E.spec[sidx].kind;
+    const bool needs_psi = kind == LGK_STATE_PEN || kind == LGK_STATE_RUN;
+    const int tg = L.tgt + si * d;
+    const int pen = L.pen + si * Wp * d;
+    const int* pc = pcol + si * Wp * d;
+    double2 a[1][W], an[1][W];
+    int col[1][W], coln[1][W];
+    const double2 ac[1][2] = {};
+    const int accol[1][2] = {};
+    if (i < d) ws_sm[tb1 + i] = E.psiN[(long)t0 * d + i];
+    team_sync(tm.id);
+    double2 ov[1] = {make_double2(0.0, 0.0)};
+    if (kind == LGK_STATE_RUN) {
+      if (i < d) ov[0] = cdot(ws_sm[tg + i], ws_sm[tb1 + i]);
+      team_reduce<1>(tm, ov, 1, red);
+    }
+    const double2 trN = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + N - 1] : make_double2(0.0, 0.0);
+    double2 cur[1][1];
+    {
+      double2 v = make_double2(0.0, 0.0);
+      if (i < d) {
+        if (kind == LGK_STATE_PEN)
+          v = pen_row(d, Wp, pen, pc, i, tb1);
+        else if (kind == LGK_STATE_RUN)
+          v = cmul(ws_sm[tg + i], ov[0]);
+        else if (kind == LGK_GATE_RUN)
+          v = cmul(ws_sm[tg + i], trN);
+        else
+          v = ws_sm[tg + i];
+      }
+      cur[0][0] = v;
+    }
+    team_sync(tm.id);
+    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+    int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
+    for (int it = 0; it < N; ++it) {
+      const int n = N - 1 - it;
+      const int slot = it % RING, use = it / RING;
+      if (use > 0) mb_wait_cl(&lempty[si * RING + slot], (use - 1) & 1);
+      if (i < d) {
+        ws_sm[tb0 + i] = cur[0][0];
+        for (int r = 1; r <= Kc; ++r) cl_st(cl_map(&ws_sm[L.lring + (si * RING + slot) * d + i], r), cur[0][0]);
+      }
+      for (int r = 1; r <= Kc; ++r) cl_arrive(cl_map(&lfull[si * RING + slot], r));
+      if (n == 0) break;
+      const int4 pl = pln;
+#pragma unroll
+      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+      load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+      pln = E.plan[(long)(n - 1) * (Kc + 1)];
+      const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
+      team_sync(tm.id);
+      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (needs_psi) {
+        mb_wait_cl(&pfull[slot], use & 1);
+        const int psi = L.ring + slot * d;
+        if (kind == LGK_STATE_RUN) {
+          double2 o2[1] = {make_double2(0.0, 0.0)};
+          if (i < d) o2[0] = cdot(ws_sm[tg + i], ws_sm[psi + i]);
+          team_reduce<1>(tm, o2, 1, red);
+          if (i < d) cur[0][0] = cadd(cur[0][0], cmul(ws_sm[tg + i], o2[0]));
+        } else {
+          if (i < d) cur[0][0] = cadd(cur[0][0], pen_row(d, Wp, pen, pc, i, psi));
+        }
+        team_sync(tm.id);
+        if (tl == 0) mb_arrive(&pempty[slot]);
+      } else if (kind == LGK_GATE_RUN) {
+        if (i < d) cur[0][0] = cadd(cur[0][0], cmul(ws_sm[tg + i], tr));
+      }
+    }
+  }
+  __syncthreads();
+  cl_sync();  // no CTA leaves while its shared memory may still be addressed remotely
+}
+
 extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp) { return ws_layout(d, nteams, I, Wp).words; }
 
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl) {
-#define LG_WS(W_, R_) \
-  if (W == W_ && rpl == R_) return backward ? (void*)lg_k_ws_backward<W_, R_> : (void*)lg_k_ws_forward<W_, R_>;
-  LG_WS(1, 1) LG_WS(2, 1) LG_WS(3, 1) LG_WS(4, 1) LG_WS(5, 1) LG_WS(6, 1) LG_WS(7, 1) LG_WS(8, 1) LG_WS(9, 1)
-  LG_WS(1, 2) LG_WS(2, 2) LG_WS(3, 2) LG_WS(4, 2) LG_WS(5, 2) LG_WS(6, 2) LG_WS(7, 2) LG_WS(8, 2) LG_WS(9, 2)
+  (void)rpl;
+#define LG_WS(W_)                                                                               \
+  if (W == W_)                                                                                  \
+    return backward == 2 ? (void*)lg_k_wsc_backward<W_>                                         \
+                         : (backward ? (void*)lg_k_ws_backward<W_> : (void*)lg_k_ws_forward<W_>);
+  LG_WS(1) LG_WS(2) LG_WS(3) LG_WS(4) LG_WS(5) LG_WS(6) LG_WS(7) LG_WS(8) LG_WS(9)
 #undef LG_WS
   return nullptr;
 }

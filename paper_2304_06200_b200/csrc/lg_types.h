@@ -92,6 +92,7 @@ struct LgEngineArgs {
   double2* trp;             // [n_specs][N][T_total]
   double2* psiN;            // [T_total][d] final states (forward -> backward)
   const double2* trsum;     // [n_specs][N] trace sums (GATE_RUN), filled between sweeps
+  long long* trace;         // optional: per-team clock64 trace [group][team][N][4] (LG_TRACE)
 };
 
 struct LgFinalArgs {
