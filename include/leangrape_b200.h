@@ -147,6 +147,10 @@ int lg_set_stream(lg_problem* p, void* stream);
 int lg_set_timing(lg_problem* p, int enable);
 int lg_get_timing(lg_problem* p, double* phase_ms /* [4] */, int64_t* evals);
 
+/* Benchmark hook: time the dense Taylor-term GEMM (lg_k_zgemm_taylor, the c5
+ * operator-term) on random data, d x d times d x C complex; ms per launch. */
+int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms_per_launch);
+
 int lg_device_count(void);
 const char* lg_last_error(void);
 const char* lg_version(void);

@@ -28,7 +28,7 @@ EXPORTED = (
     "lg_problem_create", "lg_problem_destroy", "lg_eval", "lg_cost", "lg_eval_device", "lg_plan_table",
     "lg_forward_states", "lg_raw_size", "lg_raw_get", "lg_finalize_host", "lg_make_plan",
     "lg_make_plans_device", "lg_finalize_raw", "lg_np_cabs_host", "lg_np_pairwise_host", "lg_np_reduce_host",
-    "lg_set_stream", "lg_set_timing", "lg_get_timing", "lg_device_count", "lg_last_error", "lg_version",
+    "lg_set_stream", "lg_set_timing", "lg_get_timing", "lg_bench_zgemm", "lg_device_count", "lg_last_error", "lg_version",
 )
 
 
@@ -110,6 +110,7 @@ def load() -> C.CDLL:
     lib.lg_np_reduce_host.argtypes = [C.c_int64, dp]
     lib.lg_np_reduce_host.restype = C.c_double
     lib.lg_set_stream.argtypes = [P, C.c_void_p]
+    lib.lg_bench_zgemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, dp]
     lib.lg_set_timing.argtypes = [P, C.c_int]
     lib.lg_get_timing.argtypes = [P, dp, i64p]
     lib.lg_device_count.argtypes = []

@@ -1673,6 +1673,41 @@ int lg_problem_create(const lg_problem_desc* desc, lg_problem** out) {
 
 void lg_problem_destroy(lg_problem* p) { delete p; }
 
+int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms) {
+  lg_problem tmp;
+  tmp.d = d;
+  CK(cudaStreamCreate(&tmp.stream));
+  DevMem m;
+  double* Ar = m.alloc<double>((size_t)d * d);
+  double* Ai = m.alloc<double>((size_t)d * d);
+  double2* X = m.alloc<double2>((size_t)d * C);
+  double2* cur = m.alloc<double2>((size_t)d * C);
+  double2* T = m.alloc<double2>((size_t)d * C);
+  if (!Ar || !Ai || !X || !cur || !T) {
+    m.release();
+    return fail(LG_CUDA_ERROR, "allocation failed");
+  }
+  cudaMemset(Ar, 0, sizeof(double) * d * d);
+  cudaMemset(Ai, 0, sizeof(double) * d * d);
+  cudaMemset(X, 0, sizeof(double2) * d * C);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int rc = LG_OK;
+  for (int it = 0; it < 3 && !rc; ++it) rc = dense_gemm(&tmp, Ar, Ai, X, nullptr, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
+  cudaEventRecord(e0, tmp.stream);
+  for (int it = 0; it < iters && !rc; ++it) rc = dense_gemm(&tmp, Ar, Ai, X, nullptr, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
+  cudaEventRecord(e1, tmp.stream);
+  cudaEventSynchronize(e1);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, e0, e1);
+  *ms = t / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  m.release();
+  return rc;
+}
+
 int lg_set_stream(lg_problem* p, void* stream) {
   if (!p) return fail(LG_INVALID_ARG, "null problem handle");
   CK(cudaStreamSynchronize(p->stream));
