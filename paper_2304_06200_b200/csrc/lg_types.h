@@ -93,6 +93,12 @@ struct LgEngineArgs {
   double2* psiN;            // [T_total][d] final states (forward -> backward)
   const double2* trsum;     // [n_specs][N] trace sums (GATE_RUN), filled between sweeps
   long long* trace;         // optional: per-team clock64 trace [group][team][N][4] (LG_TRACE)
+  // cluster engine (lg_sweep_cl.cu): RCM renumbering of the rows
+  int cl_R, cl_H;           // rows per CTA, halo width (bandwidth of the renumbered pattern)
+  const int* cl_perm;       // [d] renumbered row -> original row
+  const int* cl_inv;        // [d] original row -> renumbered row
+  const int* cl_cols;       // [W][d] renumbered column of slot w of renumbered row i
+  const int* cl_accols;     // [Kc][Wc][d] same for the control generators
 };
 
 struct LgFinalArgs {
