@@ -29,6 +29,7 @@ UNITS = {
     "lg_sweep_cta.cu": ["-DLG_DEBUG"] if os.environ.get("LG_DEBUG") else [],
     "lg_dense.cu": [],
     "lg_sweep_ws.cu": [],
+    "lg_sweep_cl.cu": [],
 }
 
 
