@@ -40,7 +40,7 @@ extern "C" void* lg_gather_kernel();
 extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 extern "C" void* lg_zgemm_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc);
-extern "C" int lg_cl_smem_words(int R, int H, int cmax);
+extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
 extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp);
 extern "C" void* lg_dense_form_kernel();
@@ -254,7 +254,7 @@ struct lg_problem {
   int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
   bool ws_cluster = false;
   // cluster engine
-  int cl_CS = 0, cl_R = 0, cl_H = 0, cl_maxc = 0, cl_smem = 0;
+  int cl_CS = 0, cl_R = 0, cl_H = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
   long scratch_per_group = 0;
@@ -582,6 +582,7 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.trace = nullptr;
   E.cl_R = p->cl_R;
   E.cl_H = p->cl_H;
+  E.cl_acs = 0;
   E.cl_perm = p->d_cl_perm;
   E.cl_inv = p->d_cl_inv;
   E.cl_cols = p->d_cl_cols;
@@ -1062,11 +1063,12 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     bsm = p->ws_bwd_smem;
     bblock = dim3(p->ws_bwd_threads);
   }
-  auto cl_launch = [&](void* f) -> int {
+  auto cl_launch = [&](void* f, bool backward) -> int {
+    E.cl_acs = backward ? p->cl_acs : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p->n_groups * p->cl_CS);
     cfg.blockDim = dim3(p->threads);
-    cfg.dynamicSmemBytes = p->cl_smem;
+    cfg.dynamicSmemBytes = backward ? p->cl_smem_b : p->cl_smem;
     cfg.stream = p->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1083,7 +1085,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     fwd = lg_cl_kernel(0, p->W, p->cl_maxc);
     bwd = lg_cl_kernel(1, p->W, p->cl_maxc);
   }
-  if (p->n_groups > 0) rc = p->engine == 5 ? cl_launch(fwd) : launch(fwd, grid, block, eargs, fsm, p->stream, p->multi);
+  if (p->n_groups > 0) rc = p->engine == 5 ? cl_launch(fwd, false) : launch(fwd, grid, block, eargs, fsm, p->stream, p->multi);
   if (rc) return rc;
   p->mark(2);
   if (grad && S > 0 && p->n_groups > 0) {
@@ -1093,7 +1095,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
     if (rc) return rc;
     if (p->engine == 5) {
-      rc = cl_launch(bwd);
+      rc = cl_launch(bwd, true);
       if (rc) return rc;
     } else if (p->engine == 4 && p->ws_cluster) {
       cudaLaunchConfig_t cfg{};
@@ -1227,21 +1229,25 @@ bool configure_cl(lg_problem* p, int smem_optin) {
     CS = 8;
     R = (int)((d + CS - 1) / CS);
   }
-  if (R > 640 || R < H) return false;
-  const int words = lg_cl_smem_words(R, H, cmax);
-  if ((long)words * 16 > std::min(smem_optin, 227 * 1024)) return false;
+  if (R > 640 || R < H || H > 127) return false;
+  const long cap = std::min(smem_optin, 227 * 1024);
+  const int words = lg_cl_smem_words(R, H, cmax, p->W, 0);
+  if ((long)words * 16 > cap) return false;
+  int words_b = lg_cl_smem_words(R, H, cmax, p->W, p->Kc * p->Wc);
+  const bool acs = (long)words_b * 16 <= cap && !std::getenv("LG_CL_NOACS");
+  if (!acs) words_b = words;
   void* f0 = lg_cl_kernel(0, p->W, maxc);
   void* f1 = lg_cl_kernel(1, p->W, maxc);
   if (!f0 || !f1) return false;
-  for (void* f : {f0, f1}) {
-    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, words * 16) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, words * 16) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) != cudaSuccess) return false;
+  for (void* f : {f0, f1})
     if (CS > 8 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
-  }
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(32 * ((R + 31) / 32));
-    cfg.dynamicSmemBytes = words * 16;
+    cfg.dynamicSmemBytes = words_b * 16;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CS;
@@ -1281,6 +1287,8 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_H = H;
   p->cl_maxc = maxc;
   p->cl_smem = words * 16;
+  p->cl_smem_b = words_b * 16;
+  p->cl_acs = acs ? 1 : 0;
   p->cta_Imax = Imax;
   p->threads = 32 * ((R + 31) / 32);
   p->n_slabs = 1;

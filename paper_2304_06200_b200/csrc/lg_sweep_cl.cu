@@ -71,16 +71,21 @@ struct Cl {
   int orig;                             // original row perm[gi]
   int red, rt, tb0, tb1, st, nx;        // smem offsets (double2)
   int Cmax, Cst, Wc;
+  int acs, accs;                        // staged control rows: double2 [Kc][Wc][R] and int [Kc][Wc][R] (-1: not staged)
+  int cols;                             // packed slot columns, unsigned [(W+3)/4][R]
 };
 
 template <int W, int MAXC>
 struct ClRegs {
   double2 a[W];
-  unsigned col[(W + 1) / 2];  // window-local indices, two 16-bit halves per word
   double2 cur[MAXC];
-  int koff[MAXC];             // channel offset k*Wc*d of a top column's control rows (read through L1)
-  __device__ __forceinline__ int cl(int w) const { return (int)((col[w >> 1] >> ((w & 1) * 16)) & 0xffffu); }
 };
+// Column of slot w relative to the own row (signed 8-bit, four per word) lives in a
+// thread-private shared table [(W+3)/4][R]: kept in registers it spills (L1 is
+// almost all carved out to shared memory, so spills go to L2).
+__device__ __forceinline__ int slot_col(unsigned word, int w, int base) {
+  return base + (int)(signed char)((word >> ((w & 3) * 8)) & 0xffu);
+}
 
 // Store a value of owned row li into column `colo` of window buffer `buf`
 // locally and into the halo slots of the neighbours that need it.
@@ -130,14 +135,35 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
     if (q >= C) break;
     double2 p = make_double2(0.0, 0.0), pq = make_double2(0.0, 0.0);
     if (c.own) {
-      const int xc = X + q * c.WIN;
+      const int xc = X + q * c.WIN + c.H + c.li;
+      double2 p1 = make_double2(0.0, 0.0), pq1 = make_double2(0.0, 0.0);
+      const unsigned* ct = reinterpret_cast<const unsigned*>(cl_sm + c.cols) + c.li;
+      unsigned cw[(W + 3) / 4];
 #pragma unroll
-      for (int w = 0; w < W; ++w) cmac(p, pq, R.a[w], cl_sm[xc + R.cl(w)]);
+      for (int k = 0; k < (W + 3) / 4; ++k) cw[k] = ct[k * c.R];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const double2 x = cl_sm[slot_col(cw[w >> 2], w, xc)];
+        if ((w & 1) && MAXC <= 3)
+          cmac(p1, pq1, R.a[w], x);
+        else
+          cmac(p, pq, R.a[w], x);
+      }
+      p = cadd(p, p1);
+      pq = cadd(pq, pq1);
       if (mode == 1 && q < G) {
-        const int bc = X + G * c.WIN - c.g0 + c.H;
-        const double2* ac = E.Ac + R.koff[q] + c.orig;
-        const int* acc = E.cl_accols + R.koff[q] + c.gi;
-        for (int w = 0; w < c.Wc; ++w) cmac(p, pq, __ldg(ac + w * c.d), cl_sm[bc + __ldg(acc + w * c.d)]);
+        const int koff = reinterpret_cast<const int*>(cl_sm + c.rt + 64)[q];
+        if (c.acs >= 0) {
+          const int bc = X + G * c.WIN;
+          const double2* ac = cl_sm + c.acs + koff + c.li;
+          const int* acc = reinterpret_cast<const int*>(cl_sm + c.accs) + koff + c.li;
+          for (int w = 0; w < c.Wc; ++w) cmac(p, pq, ac[w * c.R], cl_sm[bc + acc[w * c.R]]);
+        } else {
+          const int bc = X + G * c.WIN - c.g0 + c.H;
+          const double2* ac = E.Ac + koff + c.orig;
+          const int* acc = E.cl_accols + koff + c.gi;
+          for (int w = 0; w < c.Wc; ++w) cmac(p, pq, __ldg(ac + w * c.d), cl_sm[bc + __ldg(acc + w * c.d)]);
+        }
       }
     }
     const double2 tt = make_double2((p.x + pq.x) * r, (p.y + pq.y) * r);
@@ -173,17 +199,22 @@ __device__ __forceinline__ void load_row(const LgEngineArgs& E, const Cl& c, int
   for (int w = 0; w < W; ++w) R.a[w] = c.own ? src[(long)w * E.d + c.orig] : make_double2(0.0, 0.0);
 }
 template <int W, int MAXC>
-__device__ __forceinline__ void load_cols(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC>& R) {
+__device__ __forceinline__ void load_cols(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC>&) {
+  if (c.li >= c.R) return;
+  unsigned* ct = reinterpret_cast<unsigned*>(cl_sm + c.cols) + c.li;
 #pragma unroll
-  for (int w = 0; w < (W + 1) / 2; ++w) R.col[w] = 0;
+  for (int k = 0; k < (W + 3) / 4; ++k) {
+    unsigned v = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    const unsigned v = c.own ? (unsigned)(E.cl_cols[w * E.d + c.gi] - c.g0 + c.H) : (unsigned)c.H;
-    R.col[w >> 1] |= v << ((w & 1) * 16);
+    for (int w = 4 * k; w < 4 * k + 4 && w < W; ++w) {
+      const int rel = c.own ? E.cl_cols[w * E.d + c.gi] - c.gi : 0;  // |rel| <= H <= 127 (host check)
+      v |= ((unsigned)rel & 0xffu) << ((w & 3) * 8);
+    }
+    ct[k * c.R] = v;
   }
 }
 
-__device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst) {
+__device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst, int W) {
   Cl c;
   c.d = E.d;
   c.CS = (int)cl_size();
@@ -202,11 +233,21 @@ __device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst) 
   int o = 0;
   c.red = o;
   o += 16 * 32 + 16 * 16;
-  c.rt = o;
-  o += 64;
+  c.rt = o;  // [64] 1/(s j) table, then [16] int channel offsets of the aux top columns
+  o += 72;
   c.tb0 = o;
   o += Cmax * c.WIN;
   c.tb1 = o;
+  o += Cmax * c.WIN;
+  c.cols = o;
+  o += ((W + 3) / 4 * c.R + 3) / 4;
+  c.acs = c.accs = -1;
+  if (E.cl_acs) {
+    const int n = E.Kc * E.Wc * c.R;
+    c.acs = o;
+    o += n;
+    c.accs = o;
+  }
   c.st = c.nx = 0;
   return c;
 }
@@ -231,7 +272,7 @@ __global__ void __launch_bounds__(640, 1) lg_k_cl_forward(const __grid_constant_
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
   const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
-  Cl c = make_cl(E, cmax, cst);
+  Cl c = make_cl(E, cmax, cst, W);
   ClRegs<W, MAXC> R;
   load_cols<W, MAXC>(E, c, R);
   for (int q = threadIdx.x; q < 2 * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
@@ -310,10 +351,15 @@ __global__ void __launch_bounds__(640, 1) lg_k_cl_backward(const __grid_constant
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
   const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
-  Cl c = make_cl(E, cmax, cst);
+  Cl c = make_cl(E, cmax, cst, W);
   ClRegs<W, MAXC> R;
   load_cols<W, MAXC>(E, c, R);
   for (int q = threadIdx.x; q < 2 * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
+  if (c.acs >= 0 && c.li < c.R)
+    for (int kw = 0; kw < Kc * E.Wc; ++kw) {
+      cl_sm[c.acs + kw * c.R + c.li] = c.own ? E.Ac[(long)kw * c.d + c.orig] : make_double2(0.0, 0.0);
+      reinterpret_cast<int*>(cl_sm + c.accs)[kw * c.R + c.li] = c.own ? E.cl_accols[(long)kw * c.d + c.gi] - c.g0 + c.H : c.H;
+    }
   cl_sync();
   // state: psi (column 0) and the costates lambda_s (columns 1 + s), own rows in registers
   double2 psi = c.own ? E.psiN[(long)t0 * c.d + c.orig] : make_double2(0.0, 0.0);
@@ -399,12 +445,10 @@ __global__ void __launch_bounds__(640, 1) lg_k_cl_backward(const __grid_constant
         put(c, c.tb0, G, psip);
       }
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        R.cur[q] = q == G ? psip : make_double2(0.0, 0.0);
-        const int k = q < G ? gch[q] : 0;
-        const long idx = (long)k * E.Wc * c.d;
-        R.koff[q] = c.own ? (int)idx : 0;
-      }
+      for (int q = 0; q < MAXC; ++q) R.cur[q] = q == G ? psip : make_double2(0.0, 0.0);
+      if (threadIdx.x < G)  // channel offsets of the top columns (read by chain() after its cluster barrier)
+        reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] =
+            gch[threadIdx.x] * E.Wc * (c.acs >= 0 ? c.R : c.d);
       chain<W, MAXC>(E, c, R, G + 1, 1, G, pk.x, pk.y, 1.0);
       double2 v[16];
       const int nv = I * G;
@@ -468,7 +512,10 @@ __global__ void __launch_bounds__(640, 1) lg_k_cl_backward(const __grid_constant
   cl_sync();
 }
 
-extern "C" int lg_cl_smem_words(int R, int H, int cmax) { return 16 * 32 + 16 * 16 + 64 + 2 * cmax * (R + 2 * H); }
+// acw = Kc * Wc when the backward kernel stages the control-generator rows, else 0.
+extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw) {
+  return 16 * 32 + 16 * 16 + 72 + 2 * cmax * (R + 2 * H) + ((W + 3) / 4 * R + 3) / 4 + acw * R + (acw * R + 3) / 4;
+}
 
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc) {
 #define LG_CL(W_, C_) \
