@@ -196,7 +196,7 @@ template <int W, int MAXC>
 __device__ __forceinline__ void load_row(const LgEngineArgs& E, const Cl& c, int n, ClRegs<W, MAXC>& R) {
   const double2* src = E.A + (long)n * W * E.d;
 #pragma unroll
-  for (int w = 0; w < W; ++w) R.a[w] = c.own ? src[(long)w * E.d + c.orig] : make_double2(0.0, 0.0);
+  for (int w = 0; w < W; ++w) R.a[w] = c.own ? src[(long)E.cl_slot[(long)w * E.d + c.gi] * E.d + c.orig] : make_double2(0.0, 0.0);
 }
 template <int W, int MAXC>
 __device__ __forceinline__ void load_cols(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC>&) {

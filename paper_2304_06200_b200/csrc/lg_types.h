@@ -99,6 +99,7 @@ struct LgEngineArgs {
   const int* cl_perm;       // [d] renumbered row -> original row
   const int* cl_inv;        // [d] original row -> renumbered row
   const int* cl_cols;       // [W][d] renumbered column of slot w of renumbered row i
+  const unsigned char* cl_slot;  // [W][d] source ELL slot of engine slot w (bank-conflict-free order)
   const int* cl_accols;     // [Kc][Wc][d] same for the control generators
 };
 
