@@ -118,6 +118,27 @@ int64_t lg_raw_size(lg_problem* p, int64_t n_steps);
 int lg_raw_get(lg_problem* p, double* raw);
 int lg_finalize_host(lg_problem* p, int64_t n_steps, const double* raw, double* cost, double* grad);
 
+/* Multi-GPU: one process per GPU, each holding the problem created with its
+ * shard [shard_begin, shard_end) of the trajectory block (north_star: "the
+ * K-state block shards across the GPUs ... one allreduce per evaluation").
+ * The library calls `allreduce` (sum, in place, on device memory, ordered on
+ * `stream`) at the points where the shards exchange data:
+ *   - between the sweeps, the running gate traces (only if a
+ *     LG_GATE_RUNNING_INFIDELITY term is present: its costate source needs the
+ *     global traces, src/costs.py:462,477-478);
+ *   - after the backward sweep, the raw per-trajectory scalars, before the
+ *     device combine (src/costs.py:484-487, 543-544).
+ * Every rank must make the same sequence of calls.  Returns 0 on success.
+ * With lg_set_raw_buffer the raw scalars live in caller-owned device memory
+ * (e.g. a torch tensor of lg_raw_size doubles), so the hook can hand views of
+ * it straight to NCCL. */
+typedef int (*lg_allreduce_fn)(double* d_buf, int64_t count, void* stream, void* user);
+int lg_set_raw_buffer(lg_problem* p, double* d_raw, int64_t len);
+int lg_eval_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amps, lg_allreduce_fn allreduce,
+                    void* user, double* cost, double* grad);
+int lg_cost_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amps, lg_allreduce_fn allreduce,
+                    void* user, double* cost);
+
 /* make_plan (src/expm.py:279-303) on the host: bit-identical to the reference. */
 int lg_make_plan(double norm1, int64_t sigma_prime, double tau, int32_t m_max, int32_t s_max, int32_t* order,
                  int32_t* scaling, double* bound);

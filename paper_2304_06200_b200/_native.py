@@ -73,6 +73,10 @@ class lg_problem_desc(C.Structure):
 _lib = None
 
 
+# int (*lg_allreduce_fn)(double* d_buf, int64_t count, void* stream, void* user)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
 def load() -> C.CDLL:
     """Load (once) the in-tree library; raises if it was not built."""
     global _lib
@@ -100,6 +104,9 @@ def load() -> C.CDLL:
     lib.lg_raw_size.restype = C.c_int64
     lib.lg_raw_get.argtypes = [P, dp]
     lib.lg_finalize_host.argtypes = [P, C.c_int64, dp, dp, dp]
+    lib.lg_set_raw_buffer.argtypes = [P, C.c_void_p, C.c_int64]
+    lib.lg_eval_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp, dp]
+    lib.lg_cost_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp]
     lib.lg_make_plan.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_int32, C.c_int32, i32p, i32p, dp]
     lib.lg_make_plans_device.argtypes = [C.c_int64, dp, i64p, C.c_double, i32p, i32p, i32p, i32p]
     lib.lg_finalize_raw.argtypes = [C.c_int32, i32p, dp, i32p, i32p, C.c_int64, C.c_int32, C.c_int32, dp, dp, dp]

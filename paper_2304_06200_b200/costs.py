@@ -350,6 +350,34 @@ class NativeProblem:
         _native.check(self._lib.lg_raw_get(self.handle, _native.dptr(buf)))
         return buf
 
+    def raw_size(self, n_steps: int) -> int:
+        return int(self._lib.lg_raw_size(self.handle, n_steps))
+
+    def set_raw_buffer(self, ptr: int, length: int) -> None:
+        """Lend the library device memory for the raw scalars (lg_set_raw_buffer)."""
+        _native.check(self._lib.lg_set_raw_buffer(self.handle, C.c_void_p(ptr or None), int(length)))
+
+    def set_stream(self, stream_ptr: int) -> None:
+        _native.check(self._lib.lg_set_stream(self.handle, C.c_void_p(stream_ptr or None)))
+
+    def grad_sharded(self, a: ControlField, hook) -> GradientResult:
+        """lg_eval_sharded: `hook(ptr, count)` sums `count` doubles at device address ptr across ranks."""
+        amps = np.ascontiguousarray(a.amplitudes, np.float64)
+        cost = C.c_double()
+        g = np.zeros((a.n_steps, a.n_channels))
+        cb = _native.ALLREDUCE_FN(lambda ptr, count, stream, user: hook(ptr, count))
+        _native.check(self._lib.lg_eval_sharded(self.handle, a.n_steps, float(a.dt), _native.dptr(amps), cb, None,
+                                                C.byref(cost), _native.dptr(g)))
+        return GradientResult(cost=float(cost.value), grad=g, live_vector_peak=0)
+
+    def cost_sharded(self, a: ControlField, hook) -> float:
+        amps = np.ascontiguousarray(a.amplitudes, np.float64)
+        cost = C.c_double()
+        cb = _native.ALLREDUCE_FN(lambda ptr, count, stream, user: hook(ptr, count))
+        _native.check(self._lib.lg_cost_sharded(self.handle, a.n_steps, float(a.dt), _native.dptr(amps), cb, None,
+                                                C.byref(cost)))
+        return float(cost.value)
+
     def finalize(self, n_steps: int, raw: np.ndarray):
         raw = np.ascontiguousarray(raw, np.float64)
         cost = C.c_double()

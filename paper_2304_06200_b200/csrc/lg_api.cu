@@ -292,6 +292,15 @@ struct lg_problem {
   int4* d_plan = nullptr;
   int* d_flag = nullptr;
   double2 *d_ip = nullptr, *d_fin = nullptr, *d_trp = nullptr, *d_trsum = nullptr, *d_psiN = nullptr;
+  // sharded evaluation: raw scalars [ip | fin | trp | run] in one (optionally caller-lent) buffer and
+  // the caller's all-reduce hook (lg_eval_sharded)
+  double* d_raw = nullptr;
+  double* ext_raw = nullptr;
+  long ext_raw_len = 0;
+  lg_allreduce_fn hook = nullptr;
+  void* hook_user = nullptr;
+  bool trp_reduced = false;
+  bool has_gate_run = false;
   double *d_run = nullptr, *d_grad = nullptr, *d_cost = nullptr;
   int *d_spec_t0 = nullptr, *d_spec_K = nullptr;
   long lastN = 0;
@@ -410,10 +419,12 @@ int ensure_N(lg_problem* p, long N) {
   p->d_psp = m.alloc<long long>((size_t)N * (Kc + 1));
   p->d_plan = m.alloc<int4>((size_t)N * (Kc + 1));
   p->d_flag = m.alloc<int>(1);
-  p->d_ip = m.alloc<double2>((size_t)N * std::max(S, 1) * Kc * std::max(T, 1));
-  p->d_fin = m.alloc<double2>((size_t)std::max(S, 1) * std::max(T, 1));
-  p->d_run = m.alloc<double>((size_t)std::max(S, 1) * std::max(T, 1));
-  p->d_trp = m.alloc<double2>((size_t)std::max(S, 1) * N * std::max(T, 1));
+  {
+    // [ip | fin | trp | run], the lg_raw_get layout, so one all-reduce covers a shard's scalars
+    const size_t Sx = std::max(S, 1), Tx = std::max(T, 1);
+    const size_t nip = (size_t)N * Sx * Kc * Tx, nfin = Sx * Tx, ntrp = Sx * N * Tx, nrun = Sx * Tx;
+    p->d_raw = m.alloc<double>(2 * (nip + nfin + ntrp) + nrun);
+  }
   p->d_trsum = m.alloc<double2>((size_t)std::max(S, 1) * N);
   p->d_psiN = m.alloc<double2>((size_t)std::max(T, 1) * d);
   p->d_grad = m.alloc<double>((size_t)N * Kc);
@@ -838,10 +849,27 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
       trp((size_t)std::max(S, 1) * N * std::max(Tt, 1), make_double2(0, 0));
   std::vector<double> run((size_t)std::max(S, 1) * std::max(Tt, 1), 0.0);
   std::vector<double2> dots;
+  // sharded running gate costs: every rank all-reduces the set's traces between its sweeps
+  auto trace_hook = [&](int set) -> int {
+    if (!grad || !p->hook) return LG_OK;
+    bool any = false;
+    for (int s = 0; s < S; ++s) any |= p->specs[s].set == set && p->specs[s].kind == LGK_GATE_RUN;
+    if (!any) return LG_OK;
+    CK(cudaMemcpyAsync(p->d_trp, trp.data(), sizeof(double2) * trp.size(), cudaMemcpyHostToDevice, p->stream));
+    if (p->hook(reinterpret_cast<double*>(p->d_trp), 2 * (long)trp.size(), p->stream, p->hook_user) != 0)
+      return fail(LG_CUDA_ERROR, "all-reduce hook failed (traces)");
+    CK(cudaMemcpyAsync(trp.data(), p->d_trp, sizeof(double2) * trp.size(), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    p->trp_reduced = true;
+    return LG_OK;
+  };
   for (int set = 0; set < 2; ++set) {
     const int lo = (int)std::min<long>(p->shard_b, p->set_T[set]), hi = (int)std::min<long>(p->shard_e, p->set_T[set]);
     const int T = hi - lo;
-    if (T <= 0) continue;
+    if (T <= 0) {
+      if (int rh = trace_hook(set)) return rh;
+      continue;
+    }
     const int t0 = p->set_t0[set] + lo;  // global trajectory index of column 0
     std::vector<int> sp_idx;
     for (int s = 0; s < S; ++s)
@@ -905,6 +933,7 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
       }
     }
     CK(cudaMemcpyAsync(p->d_psiN + (long)t0 * d, p->dd_st, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
+    if (int rh = trace_hook(set)) return rh;
     if (!grad || I == 0) continue;
     // running gate traces summed over the set (trajectory order)
     std::vector<double2> trsum((size_t)S * N, make_double2(0, 0));
@@ -1027,13 +1056,60 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
 }
 
 // Steps 3-6 with amplitudes already on the device.
+// Point ip/fin/trp/run at the raw buffer with the exact layout of lg_raw_get for N steps
+// (the caller-lent buffer of lg_set_raw_buffer when one is set).
+int raw_views(lg_problem* p, long N) {
+  const long S = std::max<long>((long)p->specs.size(), 1), T = std::max(p->T_total, 1), Kc = p->Kc;
+  const long need = 2 * (N * S * Kc * T + S * T + S * N * T) + S * T;
+  double* base = p->d_raw;
+  if (p->ext_raw) {
+    if (p->ext_raw_len < need) return fail(LG_INVALID_ARG, "lent raw buffer is smaller than lg_raw_size");
+    base = p->ext_raw;
+  }
+  p->d_ip = reinterpret_cast<double2*>(base);
+  p->d_fin = p->d_ip + N * S * Kc * T;
+  p->d_trp = p->d_fin + S * T;
+  p->d_run = reinterpret_cast<double*>(p->d_trp + S * N * T);
+  return LG_OK;
+}
+
+// Sharded evaluation hook points.  Every rank reaches them in the same order.
+int hook_traces(lg_problem* p, long N) {  // between the sweeps: global running gate traces
+  p->trp_reduced = false;
+  if (!p->hook || !p->has_gate_run) return LG_OK;
+  const long S = (long)p->specs.size(), T = p->T_total;
+  if (p->hook(reinterpret_cast<double*>(p->d_trp), 2 * S * N * T, p->stream, p->hook_user) != 0)
+    return fail(LG_CUDA_ERROR, "all-reduce hook failed (traces)");
+  p->trp_reduced = true;
+  return LG_OK;
+}
+int hook_raw(lg_problem* p, long N) {  // before the combine: every shard's raw scalars
+  if (!p->hook) return LG_OK;
+  const long S = (long)p->specs.size(), T = p->T_total, Kc = p->Kc;
+  const long nipfin = 2 * (N * S * Kc * T + S * T), ntrp = 2 * S * N * T, nrun = S * T;
+  double* base = reinterpret_cast<double*>(p->d_ip);
+  int e = 0;
+  if (p->trp_reduced) {
+    e |= p->hook(base, nipfin, p->stream, p->hook_user);
+    e |= p->hook(base + nipfin + ntrp, nrun, p->stream, p->hook_user);
+  } else {
+    e |= p->hook(base, nipfin + ntrp + nrun, p->stream, p->hook_user);
+  }
+  if (e) return fail(LG_CUDA_ERROR, "all-reduce hook failed (raw scalars)");
+  return LG_OK;
+}
+
 int run_sweeps(lg_problem* p, long N, bool grad) {
   const int S = (int)p->specs.size(), T = p->T_total;
+  if (int rv = raw_views(p, N)) return rv;
+  p->trp_reduced = false;
   if (p->engine == 3) {
     p->mark(1);
     int rc = run_dense(p, N, p->cached_dt, grad);
     if (rc) return rc;
     p->mark(2);
+    rc = hook_raw(p, N);
+    if (rc) return rc;
     p->mark(3);
     LgFinalArgs F = final_args(p, N, p->d_ip, p->d_fin, p->d_run, p->d_trp, p->d_grad, p->d_cost);
     void* fargs[] = {&F};
@@ -1090,6 +1166,10 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   if (p->n_groups > 0) rc = p->engine == 5 ? cl_launch(fwd, false) : launch(fwd, grid, block, eargs, fsm, p->stream, p->multi);
   if (rc) return rc;
   p->mark(2);
+  if (grad) {
+    rc = hook_traces(p, N);
+    if (rc) return rc;
+  }
   if (grad && S > 0 && p->n_groups > 0) {
     int Ni = (int)N, Sv = S, Tv = T;
     long cnt = (long)S * N;
@@ -1129,6 +1209,8 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       }
     }
   }
+  rc = hook_raw(p, N);
+  if (rc) return rc;
   p->mark(3);
   LgFinalArgs F = final_args(p, N, p->d_ip, p->d_fin, p->d_run, p->d_trp, p->d_grad, p->d_cost);
   void* fargs[] = {&F};
@@ -1142,6 +1224,8 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
 
 int check_field(lg_problem* p, long N, double dt, const double* amps) {
   if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  if (p->has_gate_run && p->shard_e < (1L << 40) && !p->hook)
+    return fail(LG_UNSUPPORTED, "a sharded running gate cost needs lg_eval_sharded (global traces between sweeps)");
   if (N < 1) return fail(LG_INVALID_ARG, "need at least one step and one channel");
   if (!(dt > 0.0)) return fail(LG_INVALID_ARG, "dt must be positive");
   if (amps)
@@ -1732,8 +1816,7 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
     sp.kind = ct.kind;
     sp.weight = ct.weight;
     sp.set = (ct.kind <= LG_STATE_RUNNING_INFIDELITY || merged) ? 0 : 1;
-    if (sp.kind == LG_GATE_RUNNING_INFIDELITY && D->shard_end > 0)
-      return fail(LG_UNSUPPORTED, "sharded running gate cost needs the split forward/backward API");
+    if (sp.kind == LG_GATE_RUNNING_INFIDELITY) p->has_gate_run = true;
     const int K = p->set_T[sp.set];
     if (ct.kind == LG_STATE_PENALTY) {
       rc = parse_mat(ct.penalty, d, &sp.pen, "penalty operator");
@@ -2083,6 +2166,44 @@ int lg_eval(lg_problem* p, int64_t n_steps, double dt, const double* amps, doubl
   p->collect();
   if (live_vector_peak) *live_vector_peak = p->live_peak;
   return LG_OK;
+}
+
+int lg_set_raw_buffer(lg_problem* p, double* d_raw, int64_t len) {
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  if ((d_raw == nullptr) != (len == 0)) return fail(LG_INVALID_ARG, "raw buffer and length must both be set or both 0");
+  p->ext_raw = d_raw;
+  p->ext_raw_len = len;
+  return LG_OK;
+}
+
+namespace {
+struct HookScope {  // installs the caller's all-reduce hook for one call
+  lg_problem* p;
+  HookScope(lg_problem* p_, lg_allreduce_fn fn, void* user) : p(p_) {
+    p->hook = fn;
+    p->hook_user = user;
+  }
+  ~HookScope() {
+    p->hook = nullptr;
+    p->hook_user = nullptr;
+  }
+};
+}  // namespace
+
+int lg_eval_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amps, lg_allreduce_fn allreduce,
+                    void* user, double* cost, double* grad) {
+  if (!allreduce) return fail(LG_INVALID_ARG, "lg_eval_sharded needs an all-reduce hook");
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  HookScope hs(p, allreduce, user);
+  return lg_eval(p, n_steps, dt, amps, cost, grad, nullptr);
+}
+
+int lg_cost_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amps, lg_allreduce_fn allreduce,
+                    void* user, double* cost) {
+  if (!allreduce) return fail(LG_INVALID_ARG, "lg_cost_sharded needs an all-reduce hook");
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  HookScope hs(p, allreduce, user);
+  return lg_cost(p, n_steps, dt, amps, cost);
 }
 
 int lg_cost(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost) {
