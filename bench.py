@@ -125,6 +125,15 @@ def algorithmic_bytes(case, plan_table):
     return fwd_bytes + bwd_bytes, bwd_bytes, flops
 
 
+def critical_path_terms(plan_table):
+    """Sequentially dependent operator-terms of one evaluation: the forward chain
+    N*mu, then per backward step the adjoint chain mu plus the aux chain mu_aux (channels sharing a
+    plan run as one chain)."""
+    mu = plan_table["m"].astype(np.int64) * plan_table["s"]
+    mua = (plan_table["aux_m"].astype(np.int64) * plan_table["aux_s"]).max(axis=1)
+    return int(mu.sum() + mu.sum() + mua.sum())
+
+
 def cpu_reference(case, budget_s=20.0):
     """Time the oracle port of the reference algorithm on a bounded prefix (one process per
     trajectory).  Returns (evals_per_s_extrapolated, cores, sample description)."""
@@ -213,6 +222,7 @@ def run_ours(args):
 
     from paper_2304_06200_b200 import _native, composite_grad, models
     from paper_2304_06200_b200.costs import NativeProblem
+    from paper_2304_06200_b200.distributed import ShardedEvaluator
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,20 +233,40 @@ def run_ours(args):
     lib = _native.load()
     case = models.build_case(args.config)
     p = case.problem
-    states = p.initial_state
-    npb = NativeProblem(p, case.terms, initial_states=states if any(
-        t.kind.value.startswith("state") for t in case.terms) else None, basis=p.basis, device=local)
-    stream = torch.cuda.current_stream()
-    _native.check(lib.lg_set_stream(npb.handle, stream.cuda_stream))
     N, Kc = case.field.n_steps, case.field.n_channels
-    d_amps = torch.from_numpy(case.field.amplitudes).cuda()
-    d_cost = torch.zeros(1, dtype=torch.float64, device="cuda")
-    d_grad = torch.zeros((N, Kc), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    has_state = any(t.kind.value.startswith("state") for t in case.terms)
+    if args.shard:
+        # the trajectory block sharded over the ranks, one NCCL all-reduce per evaluation (strong scaling)
+        ev = ShardedEvaluator(p, case.terms, device=local)
+        npb = ev.native
+        ev._lend(N)
 
-    def dev_eval():
-        _native.check(lib.lg_eval_device(npb.handle, N, case.field.dt, d_amps.data_ptr(), d_cost.data_ptr(),
-                                         d_grad.data_ptr()))
+        def dev_eval():
+            ev.grad(case.field)
+
+        def e2e_eval():
+            return ev.grad(case.field)
+
+        share = (ev.shard[1] - ev.shard[0]) / max(ev.n_traj, 1)
+    else:
+        # replicas: every rank evaluates the whole workload (weak scaling)
+        npb = NativeProblem(p, case.terms, initial_states=p.initial_state if has_state else None, basis=p.basis,
+                            device=local)
+        _native.check(lib.lg_set_stream(npb.handle, stream.cuda_stream))
+        d_amps = torch.from_numpy(case.field.amplitudes).cuda()
+        d_cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+        d_grad = torch.zeros((N, Kc), dtype=torch.float64, device="cuda")
+
+        def dev_eval():
+            _native.check(lib.lg_eval_device(npb.handle, N, case.field.dt, d_amps.data_ptr(), d_cost.data_ptr(),
+                                             d_grad.data_ptr()))
+
+        def e2e_eval():
+            return composite_grad(case.problem, case.field, case.terms)
+
+        share = 1.0
 
     for _ in range(args.warmup):
         dev_eval()
@@ -247,6 +277,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launches0 = lib.lg_launch_count()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(float(i))
@@ -254,6 +285,7 @@ def run_ours(args):
             dev_eval()
             ends[i].record(stream)
         torch.cuda.synchronize()
+    launches = int(lib.lg_launch_count() - launches0)
     if world > 1:
         dist.barrier()
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -266,7 +298,8 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = world * args.steps / (total_ms / 1e3)
+    jobs = 1 if args.shard else world  # evaluations the whole job completes per step
+    value = jobs * args.steps / (total_ms / 1e3)
 
     # end to end through the public API with host buffers
     e2e_ms = []
@@ -274,36 +307,44 @@ def run_ours(args):
         flush.fill_(float(i))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = composite_grad(case.problem, case.field, case.terms)
+        res = e2e_eval()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * args.steps / (float(te.item()) / 1e3)
+    e2e_value = jobs * args.steps / (float(te.item()) / 1e3)
 
-    # roofline of the dominant kernel (backward sweep)
+    # roofline of the dominant kernel (the backward sweep) on this rank
     table = npb.plan_table(case.field)
     tot_bytes, bwd_bytes, flops = algorithmic_bytes(case, table)
-    bwd_ms = phase[2] / max(int(nev[0]), 1)
+    bwd_bytes *= share
+    nevals = max(int(nev[0]), 1)
+    bwd_ms = phase[2] / nevals
     peak, peak_kind = _peaks()
     achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
+    crit = critical_path_terms(table)
+    engine = lib.lg_engine_name(npb.handle).decode()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": case.name, "description": case.description, "n_steps": N,
-                   "n_states": case.n_states, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "n_states": case.n_states,
+                   "parallelism": (f"trajectory shards x{world} (NCCL all-reduce per evaluation)" if args.shard
+                                   else (f"replicas x{world}" if world > 1 else "single")),
                    "l2": "flushed (256 MiB write) between timed evaluations"},
         "state_steps_per_sec": value * case.n_states * N,
-        "phase_ms_per_eval": {k: float(v / max(int(nev[0]), 1)) for k, v in
+        "phase_ms_per_eval": {k: float(v / nevals) for k, v in
                               zip(["prep_plans", "forward", "backward", "finalize"], phase)},
-        "roofline": {"bound": "hbm", "kernel": "lg_k_backward", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": engine, "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "algorithmic_bytes_per_launch": bwd_bytes, "algorithmic_bytes_per_eval": tot_bytes,
-                     "flops_per_eval": flops},
+                     "flops_per_eval": flops,
+                     "critical_path_terms": crit,
+                     "ns_per_critical_term": 1e6 * (phase[1] + phase[2]) / nevals / max(crit, 1)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N * Kc,
                 "d2h_bytes_per_step": 8 * N * Kc + 8},
-        "gpu_launches": 7 * args.steps,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "cost": res.cost,
     }
@@ -326,6 +367,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="CPU seconds per reference sample (default: ~100 s over all steps)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="shard the trajectory block over the ranks (NCCL all-reduce per evaluation)")
     args = ap.parse_args()
     if args.ref_budget is None:
         args.ref_budget = 12.0 if args.impl == "ours" else max(2.0, 100.0 / (args.steps + args.warmup))

@@ -172,6 +172,10 @@ int lg_get_timing(lg_problem* p, double* phase_ms /* [4] */, int64_t* evals);
  * operator-term) on random data, d x d times d x C complex; ms per launch. */
 int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms_per_launch);
 
+/* "<engine>:<dominant backward kernel>" chosen for this problem (diagnostics, bench.py roofline). */
+const char* lg_engine_name(lg_problem* p);
+/* Kernels launched by this library since load (all problems, all threads; diagnostics). */
+int64_t lg_launch_count(void);
 int lg_device_count(void);
 const char* lg_last_error(void);
 const char* lg_version(void);

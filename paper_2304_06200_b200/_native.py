@@ -121,6 +121,10 @@ def load() -> C.CDLL:
     lib.lg_set_timing.argtypes = [P, C.c_int]
     lib.lg_get_timing.argtypes = [P, dp, i64p]
     lib.lg_device_count.argtypes = []
+    lib.lg_engine_name.argtypes = [P]
+    lib.lg_engine_name.restype = C.c_char_p
+    lib.lg_launch_count.argtypes = []
+    lib.lg_launch_count.restype = C.c_int64
     lib.lg_last_error.restype = C.c_char_p
     lib.lg_version.restype = C.c_char_p
     _lib = lib

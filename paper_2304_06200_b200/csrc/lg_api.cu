@@ -441,7 +441,10 @@ int ensure_N(lg_problem* p, long N) {
   return LG_OK;
 }
 
+long long g_launches = 0;  // kernels this library launched (lg_launch_count)
+
 int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop = false) {
+  ++g_launches;
   cudaError_t e = coop ? cudaLaunchCooperativeKernel(f, grid, block, args, smem, st)
                        : cudaLaunchKernel(f, grid, block, args, smem, st);
   if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -1155,6 +1158,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    ++g_launches;
     cudaError_t e = cudaLaunchKernelExC(&cfg, f, eargs);
     if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
     return LG_OK;
@@ -1192,6 +1196,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
+      ++g_launches;
       cudaError_t e = cudaLaunchKernelExC(&cfg, lg_ws_kernel(2, p->W, p->ws_rpl), eargs);
       if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
     } else {
@@ -1550,7 +1555,7 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   p->ws_rpl = rpl;
   p->ws_fwd_smem = fw * 16;
   p->ws_bwd_smem = bw * 16;
-  p->ws_bwd_threads = p->ws_cluster ? std::max(128, (1 + Imax) * 64) : (p->Kc + 1 + Imax) * 64;
+  p->ws_bwd_threads = p->ws_cluster ? std::max(160, (1 + Imax) * 64) : (p->Kc + 1 + Imax) * 64;
   if (p->ws_cluster) p->ws_bwd_smem = cw * 16;
   p->threads = 128;
   p->n_slabs = 1;
@@ -2108,6 +2113,21 @@ int lg_set_stream(lg_problem* p, void* stream) {
   p->stream = (cudaStream_t)stream;
   p->own_stream = false;
   return LG_OK;
+}
+
+int64_t lg_launch_count(void) { return g_launches; }
+
+const char* lg_engine_name(lg_problem* p) {
+  if (!p) return "none";
+  switch (p->engine) {
+    case 0: return "grid:lg_k_backward";
+    case 1: return "grid-multi:lg_k_backward";
+    case 2: return "cta:lg_k_cta_backward";
+    case 3: return "dense:lg_k_zgemm_taylor";
+    case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
+    case 5: return "cluster:lg_k_cl_backward";
+    default: return "unknown";
+  }
 }
 
 int lg_set_timing(lg_problem* p, int enable) {

@@ -72,18 +72,21 @@ __device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smaddr(p)), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void cl_st(unsigned addr, double2 v) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+// Push 16 bytes into a peer CTA's shared memory and count them on the peer's mbarrier
+// (async proxy, like a TMA store): the consumer waits with CTA-scope acquire, no L1 invalidation.
+__device__ __forceinline__ void cl_st_async(unsigned addr, double2 v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(mbar)
+               : "memory");
 }
-__device__ __forceinline__ void cl_arrive(unsigned addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+// Arm the current phase of a local mbarrier for `bytes` of incoming st.async data (one arrival).
+__device__ __forceinline__ void mb_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smaddr(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mb_wait_cl(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra "
-      "WAITC_%=;\n}\n" ::"r"(smaddr(b)),
-      "r"(parity)
-      : "memory");
+// "Slot free" signal to a peer's ring: carries no data (the slot's values were already consumed
+// into registers), so no release fence.
+__device__ __forceinline__ void cl_arrive_relaxed(unsigned addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
 }
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -256,6 +259,7 @@ struct WsLay {
   int tgt;     // targets: I x d
   int pen;     // penalty values: I x Wp x d ; cols as ints after
   int pencol;  // int offset (double2 units * 4 = int units)
+  int dbuf;    // [2][d] derivative hand-off (cluster kernel)
   int bars;    // mbarriers
   int words;
 };
@@ -279,8 +283,10 @@ __host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, in
   o += I * Wp * d;
   L.pencol = o;
   o += (I * Wp * d + 3) / 4;
+  L.dbuf = o;  // [2][d] derivative columns handed from the X team to its dot warp (cluster kernel)
+  o += 2 * d;
   L.bars = o;
-  o += (2 * RING * (1 + I) + 1) / 2 + 1;
+  o += (2 * RING * (1 + I) + 4 + 1) / 2 + 1;
   L.words = o;
   return L;
 }
@@ -689,6 +695,8 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   unsigned long long* pempty = bars + RING;       // [RING]  (rank 0)
   unsigned long long* lfull = bars + 2 * RING;    // [I][RING] (X ranks)
   unsigned long long* lempty = lfull + I * RING;  // [I][RING] (rank 0)
+  unsigned long long* dfull = lempty + I * RING;  // [2] X team -> dot warp (X ranks)
+  unsigned long long* dempty = dfull + 2;         // [2] dot warp -> X team
   int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
   const int team = threadIdx.x >> 6, tl = threadIdx.x & 63;
   const Team tm{team + 1, tl, 64, d};
@@ -699,13 +707,19 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   }
   stage_specs(E, L, set, trel, I, Wp, pcol);
   if (threadIdx.x == 0) {
+    // rank 0: pfull counts the 64 local P arrivals; X ranks: full barriers are armed by one
+    // expect_tx arrival per phase and completed by the producers' st.async bytes
     for (int j = 0; j < RING; ++j) {
-      mb_init(&pfull[j], 64);
+      mb_init(&pfull[j], rank == 0 ? 64 : 1);
       mb_init(&pempty[j], Kc + n_lpsi);
       for (int si = 0; si < I; ++si) {
-        mb_init(&lfull[si * RING + j], 64);
+        mb_init(&lfull[si * RING + j], rank == 0 ? 64 : 1);
         mb_init(&lempty[si * RING + j], Kc);
       }
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&dfull[b], 1);
+      mb_init(&dempty[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
     };
     rows(N - 1, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1) + 1 + kch];
-    const int xb0 = L.tb, xb1 = L.tb + 2 * d, xrt = L.rt, xred = L.red;
+    const int xb0 = L.tb, xb1 = L.tb + 2 * d, xrt = L.rt;
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int4 pl = pln;
@@ -753,7 +767,8 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       const int slot = it % RING, use = it / RING;
       long long* trc = E.trace ? E.trace + (((long)g * 8 + kch) * N + it) * 4 : nullptr;
       if (trc && t4 == 0) trc[0] = clock64();
-      mb_wait_cl(&pfull[slot], use & 1);
+      if (t4 == 0) mb_expect_tx(&pfull[slot], (unsigned)d * 16u);
+      mb_wait(&pfull[slot], use & 1);
       if (trc && t4 == 0) trc[1] = clock64();
       double2 cur = make_double2(0.0, 0.0);
       if (ix < d) {
@@ -762,36 +777,44 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
         ws_sm[xb0 + (top ? 0 : d) + ix] = top ? make_double2(0.0, 0.0) : v0;
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (t4 == 0) cl_arrive(cl_map(&pempty[slot], 0));
+      if (t4 == 0) cl_arrive_relaxed(cl_map(&pempty[slot], 0));
       x4_chain<W>(1, ix, d, top, cur, a, col, ac, accol, pl.x, pl.y, xb0, xb1, xrt, t4);
       if (trc && t4 == 0) trc[2] = clock64();
-      // <lambda_s(n) | D_k>: top threads hold D
-      double2 v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = make_double2(0.0, 0.0);
-      for (int si = 0; si < I; ++si) {
-        mb_wait_cl(&lfull[si * RING + slot], use & 1);
-        if (top && ix < d) v[si] = cdot(ws_sm[L.lring + (si * RING + slot) * d + ix], cur);
-      }
-      const int wq = t4 >> 5;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q >= I) break;
-        v[q] = warp_sum(v[q]);
-        if ((t4 & 31) == 0) ws_sm[xred + q * 4 + wq] = v[q];
-      }
+      // hand D_k (top column) to the dot warp; it reduces <lambda_s(n)|D_k> off this critical path
+      const int b = it & 1;
+      if (it >= 2) mb_wait(&dempty[b], ((it >> 1) - 1) & 1);
+      if (top && ix < d) ws_sm[L.dbuf + b * d + ix] = cur;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (t4 == 0) mb_arrive(&dfull[b]);
       if (trc && t4 == 0) trc[3] = clock64();
-      if (t4 == 0) {
+    }
+  } else if (rank > 0 && threadIdx.x < 160) {
+    // ---------------- dot warp of X_k: ip[n][s][k] = <lambda_s(n) | dU_n/da_k psi_{n-1}>
+    const int kch = rank - 1;
+    const int lane = threadIdx.x - 128;
+    for (int it = 0; it < N; ++it) {
+      const int n = N - 1 - it;
+      const int slot = it % RING, use = it / RING, b = it & 1;
+      if (lane < I) mb_expect_tx(&lfull[lane * RING + slot], (unsigned)d * 16u);
+      mb_wait(&dfull[b], (it >> 1) & 1);
+      double2 v[LG_MAX_SPECS];
+      for (int si = 0; si < I; ++si) {
+        mb_wait(&lfull[si * RING + slot], use & 1);
+        double2 acc = make_double2(0.0, 0.0);
+        for (int i2 = lane; i2 < d; i2 += 32)
+          acc = cadd(acc, cdot(ws_sm[L.lring + (si * RING + slot) * d + i2], ws_sm[L.dbuf + b * d + i2]));
+        v[si] = warp_sum(acc);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mb_arrive(&dempty[b]);
         for (int si = 0; si < I; ++si) {
-          const double2 r0 = cadd(cadd(ws_sm[xred + si * 4 + 0], ws_sm[xred + si * 4 + 1]),
-                                  cadd(ws_sm[xred + si * 4 + 2], ws_sm[xred + si * 4 + 3]));
-          cl_arrive(cl_map(&lempty[si * RING + slot], 0));
+          cl_arrive_relaxed(cl_map(&lempty[si * RING + slot], 0));
           const int sidx = E.set_spec[set][si];
-          E.ip[(((long)n * E.n_specs + sidx) * Kc + kch) * E.T_total + t0] = r0;
+          E.ip[(((long)n * E.n_specs + sidx) * Kc + kch) * E.T_total + t0] = v[si];
         }
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      __syncwarp();
     }
   } else if (rank == 0 && team == 0) {
     // ---------------- P: psi recovery; pushes psi_{n-1} to every X CTA
@@ -819,15 +842,15 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[1] = clock64();
       const int slot = it % RING, use = it / RING;
-      if (use > 0) mb_wait_cl(&pempty[slot], (use - 1) & 1);
+      if (use > 0) mb_wait(&pempty[slot], (use - 1) & 1);
       if (trc && tl == 0) trc[2] = clock64();
       if (i < d) {
         ws_sm[L.ring + slot * d + i] = cur[0][0];
         ws_sm[tb0 + i] = cur[0][0];
-        for (int r = 1; r <= Kc; ++r) cl_st(cl_map(&ws_sm[L.ring + slot * d + i], r), cur[0][0]);
+        for (int r = 1; r <= Kc; ++r)
+          cl_st_async(cl_map(&ws_sm[L.ring + slot * d + i], r), cur[0][0], cl_map(&pfull[slot], r));
       }
       mb_arrive(&pfull[slot]);
-      for (int r = 1; r <= Kc; ++r) cl_arrive(cl_map(&pfull[slot], r));
       team_sync(tm.id);
     }
   } else if (rank == 0 && team <= I) {
@@ -872,12 +895,13 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int slot = it % RING, use = it / RING;
-      if (use > 0) mb_wait_cl(&lempty[si * RING + slot], (use - 1) & 1);
+      if (use > 0) mb_wait(&lempty[si * RING + slot], (use - 1) & 1);
       if (i < d) {
         ws_sm[tb0 + i] = cur[0][0];
-        for (int r = 1; r <= Kc; ++r) cl_st(cl_map(&ws_sm[L.lring + (si * RING + slot) * d + i], r), cur[0][0]);
+        for (int r = 1; r <= Kc; ++r)
+          cl_st_async(cl_map(&ws_sm[L.lring + (si * RING + slot) * d + i], r), cur[0][0],
+                      cl_map(&lfull[si * RING + slot], r));
       }
-      for (int r = 1; r <= Kc; ++r) cl_arrive(cl_map(&lfull[si * RING + slot], r));
       if (n == 0) break;
       const int4 pl = pln;
 #pragma unroll
@@ -888,7 +912,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       team_sync(tm.id);
       team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (needs_psi) {
-        mb_wait_cl(&pfull[slot], use & 1);
+        mb_wait(&pfull[slot], use & 1);
         const int psi = L.ring + slot * d;
         if (kind == LGK_STATE_RUN) {
           double2 o2[1] = {make_double2(0.0, 0.0)};
