@@ -125,6 +125,20 @@ def algorithmic_bytes(case, plan_table):
     return fwd_bytes + bwd_bytes, bwd_bytes, flops
 
 
+def committed_traffic(workload, kernel, n_steps):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/r01_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum), scaled to n_steps when
+    the capture ran on a prefix.  None when no capture of this kernel/workload is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            t = json.load(fh).get(workload)
+        if not t or t["kernel"] not in kernel:
+            return None, None
+        return t["dram_bytes_per_launch"] * n_steps / t["n_steps_captured"], t["source"]
+    except Exception:
+        return None, None
+
+
 def critical_path_terms(plan_table):
     """Sequentially dependent operator-terms of one evaluation: the forward chain
     N*mu, then per backward step the adjoint chain mu plus the aux chain mu_aux (channels sharing a
@@ -324,6 +338,7 @@ def run_ours(args):
     achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
     crit = critical_path_terms(table)
     engine = lib.lg_engine_name(npb.handle).decode()
+    traffic, traffic_src = committed_traffic(case.name, engine, N) if not args.shard else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -337,7 +352,8 @@ def run_ours(args):
         "phase_ms_per_eval": {k: float(v / nevals) for k, v in
                               zip(["prep_plans", "forward", "backward", "finalize"], phase)},
         "roofline": {"bound": "hbm", "kernel": engine, "achieved": achieved, "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": bwd_bytes, "algorithmic_bytes_per_eval": tot_bytes,
                      "flops_per_eval": flops,
                      "critical_path_terms": crit,
