@@ -73,6 +73,7 @@ struct Ctx {
   int rl, cs, lane, slot;
   int W, Wc;
   bool a_smem, ac_smem;
+  bool dense;            // dense rows: slot w is column w (no index loads)
   const double2* astep;  // global A_n of the current step (global-A mode)
   Lay L;
 };
@@ -181,6 +182,19 @@ __device__ __forceinline__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG
           if (WREG > 0) {
 #pragma unroll
             for (int w = 0; w < (WREG > 0 ? WREG : 1); ++w) cmac(p, pq, R.a[k][w], SMX(xc + R.col[k][w]));
+          } else if (c.dense) {
+            // dense rows: x[w] is a broadcast read, four independent accumulator pairs
+            double2 p1 = make_double2(0.0, 0.0), q1 = p1, p2 = p1, q2 = p1, p3 = p1, q3 = p1;
+            int w = 0;
+            for (; w + 4 <= W; w += 4) {
+              cmac(p, pq, Ap[w * d + i], SMX(xc + w));
+              cmac(p1, q1, Ap[(w + 1) * d + i], SMX(xc + w + 1));
+              cmac(p2, q2, Ap[(w + 2) * d + i], SMX(xc + w + 2));
+              cmac(p3, q3, Ap[(w + 3) * d + i], SMX(xc + w + 3));
+            }
+            for (; w < W; ++w) cmac(p, pq, Ap[w * d + i], SMX(xc + w));
+            p = cadd(cadd(p, p1), cadd(p2, p3));
+            pq = cadd(cadd(pq, q1), cadd(q2, q3));
           } else {
             for (int w = 0; w < W; ++w) {
               const int q2 = w * d + i;
@@ -192,6 +206,17 @@ __device__ __forceinline__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG
             if (acreg) {
               cmac(p, pq, R.ac[q][k][0], SMX(bc + R.accol[q][k][0]));
               cmac(p, pq, R.ac[q][k][1], SMX(bc + R.accol[q][k][1]));
+            } else if (c.dense) {
+              const int base = kbase[q] + i;
+              double2 p1 = make_double2(0.0, 0.0), q1 = p1;
+              int w = 0;
+              for (; w + 2 <= Wc; w += 2) {
+                cmac(p, pq, Acp[base + w * d], SMX(bc + w));
+                cmac(p1, q1, Acp[base + (w + 1) * d], SMX(bc + w + 1));
+              }
+              for (; w < Wc; ++w) cmac(p, pq, Acp[base + w * d], SMX(bc + w));
+              p = cadd(p, p1);
+              pq = cadd(pq, q1);
             } else {
               const int base = kbase[q] + i;
               for (int w = 0; w < Wc; ++w) cmac(p, pq, Acp[base + w * d], SMX(bc + Ccp[base + w * d]));
@@ -289,6 +314,7 @@ __device__ void init(Ctx& c, double2* sm, const LgEngineArgs& E) {
   c.Wc = E.Wc;
   c.a_smem = (E.smem_mode & 4) != 0;
   c.ac_smem = (E.smem_mode & 8) != 0;
+  c.dense = E.dense_rows != 0;
   const int d = E.d, Tg = E.grp_T;
   const int cstate = Tg * (1 + E.cta_Imax), cx = (E.Kc + 1) * Tg, cmax = cstate > cx ? cstate : cx;
   int o = 0;
