@@ -139,6 +139,15 @@ int lg_eval_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amp
 int lg_cost_sharded(lg_problem* p, int64_t n_steps, double dt, const double* amps, lg_allreduce_fn allreduce,
                     void* user, double* cost);
 
+/* Standalone certified action (src/expm.py:306-369).
+ * lg_expm_plan_inputs: the planner inputs of a generator A exactly as the reference computes them
+ *   (A.one_norm() with numpy's reduction order, A.max_row_nnz(); DenseMatrix -> n), host only.
+ * lg_expm_apply: exp(A) applied to n_vec vectors (psi: [n_vec][2n], interleaved complex) under the
+ *   plan (order, scaling) -- the Taylor recursion of expm.apply on the GPU; out may alias psi. */
+int lg_expm_plan_inputs(const lg_matrix* a, double* norm1, int64_t* sigma_prime);
+int lg_expm_apply(const lg_matrix* a, int64_t n_vec, const double* psi, int32_t order, int32_t scaling,
+                  double* out, int32_t device);
+
 /* make_plan (src/expm.py:279-303) on the host: bit-identical to the reference. */
 int lg_make_plan(double norm1, int64_t sigma_prime, double tau, int32_t m_max, int32_t s_max, int32_t* order,
                  int32_t* scaling, double* bound);

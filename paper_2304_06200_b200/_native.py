@@ -105,6 +105,8 @@ def load() -> C.CDLL:
     lib.lg_raw_get.argtypes = [P, dp]
     lib.lg_finalize_host.argtypes = [P, C.c_int64, dp, dp, dp]
     lib.lg_set_raw_buffer.argtypes = [P, C.c_void_p, C.c_int64]
+    lib.lg_expm_plan_inputs.argtypes = [C.POINTER(lg_matrix), dp, i64p]
+    lib.lg_expm_apply.argtypes = [C.POINTER(lg_matrix), C.c_int64, dp, C.c_int32, C.c_int32, dp, C.c_int32]
     lib.lg_eval_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp, dp]
     lib.lg_cost_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp]
     lib.lg_make_plan.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_int32, C.c_int32, i32p, i32p, dp]

@@ -32,6 +32,17 @@
 extern "C" void* lg_forward_kernel(int multi);
 extern "C" void* lg_backward_kernel(int multi);
 extern "C" void* lg_trsum_kernel();
+extern "C" void* lg_ell_taylor_kernel();
+struct LgEllTaylorArgs {  // lg_dense.cu
+  int d, W, ncol, first, last;
+  double r;
+  const int* cols;
+  const double2* vals;
+  const double2* X;
+  const double2* xin;
+  double2* cur;
+  double2* T;
+};
 extern "C" void* lg_finalize_kernel();
 extern "C" void* lg_prep_sparse_kernel();
 extern "C" void* lg_prep_dense_kernel();
@@ -2347,6 +2358,98 @@ double lg_np_pairwise_host(int64_t n, const double* a) {
 double lg_np_reduce_host(int64_t n, const double* a) {
   auto get = [&](long k) { return a[k]; };
   return lg_np_reduce(get, 0, (long)n);
+}
+
+int lg_expm_plan_inputs(const lg_matrix* a, double* norm1, int64_t* sigma_prime) {
+  if (!a || !norm1 || !sigma_prime || a->n < 0) return fail(LG_INVALID_ARG, "null argument");
+  Mat m;
+  int rc = parse_mat(*a, a->n, &m, "generator");
+  if (rc) return rc;
+  const long n = m.n;
+  double best = 0.0;
+  if (m.dense) {
+    // abs(F-array).sum(axis=0).max(): numpy pairwise per contiguous column (src/sparse.py:201-222)
+    std::vector<double> col((size_t)n);
+    for (long j = 0; j < n; ++j) {
+      for (long i = 0; i < n; ++i) col[i] = lg_np_cabs(m.vals[(size_t)j * n + i].x, m.vals[(size_t)j * n + i].y);
+      auto get = [&](long k) { return col[k]; };
+      const double sj = lg_np_pairwise(get, 0, n);
+      best = (j == 0 || sj > best) ? sj : best;
+    }
+    *sigma_prime = n;  // DenseMatrix.max_row_nnz returns n_cols
+  } else {
+    // np.bincount(col, |v|, minlength=n).max(): sequential per column in CSR order (src/sparse.py:90-121)
+    std::vector<double> cs((size_t)n, 0.0);
+    for (size_t k = 0; k < m.indices.size(); ++k) cs[m.indices[k]] += lg_np_cabs(m.vals[k].x, m.vals[k].y);
+    for (long j = 0; j < n; ++j) best = (j == 0 || cs[j] > best) ? cs[j] : best;
+    long sp = 0;
+    for (long i = 0; i < n; ++i) sp = std::max(sp, m.indptr[i + 1] - m.indptr[i]);
+    *sigma_prime = sp;
+  }
+  *norm1 = best;
+  return LG_OK;
+}
+
+int lg_expm_apply(const lg_matrix* a, int64_t n_vec, const double* psi, int32_t order, int32_t scaling,
+                  double* out, int32_t device) {
+  if (!a || !psi || !out || n_vec < 1 || order < 0 || scaling < 1) return fail(LG_INVALID_ARG, "bad arguments");
+  Mat m;
+  int rc = parse_mat(*a, a->n, &m, "generator");
+  if (rc) return rc;
+  const long d = m.n;
+  if (d < 1) return fail(LG_INVALID_ARG, "empty generator");
+  if (order == 0) {  // zero generator plan: exp(A) psi = psi
+    std::memcpy(out, psi, sizeof(double2) * d * n_vec);
+    return LG_OK;
+  }
+  int W = 1;
+  std::vector<int> cols;
+  std::vector<double2> vals;
+  to_ell(m, &W, cols, vals, nullptr);
+  CK(cudaSetDevice(device));
+  DevMem mem;
+  const int* dcols = mem.upload(cols);
+  const double2* dvals = mem.upload(vals);
+  std::vector<double2> h((size_t)d * n_vec);
+  std::memcpy(h.data(), psi, sizeof(double2) * h.size());
+  const double2* dpsi = mem.upload(h);
+  double2* cur = mem.alloc<double2>(h.size());
+  double2* t0 = mem.alloc<double2>(h.size());
+  double2* t1 = mem.alloc<double2>(h.size());
+  if (!dcols || !dvals || !dpsi || !cur || !t0 || !t1) return fail(LG_CUDA_ERROR, "device allocation failed");
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  LgEllTaylorArgs A{};
+  A.d = (int)d;
+  A.W = W;
+  A.ncol = (int)n_vec;
+  A.cols = dcols;
+  A.vals = dvals;
+  A.xin = dpsi;
+  A.cur = cur;
+  const double2* x = dpsi;
+  double2* outs[2] = {t0, t1};
+  int k = 0;
+  const dim3 grid((unsigned)std::min<long>((d + 255) / 256, 1024), (unsigned)n_vec);
+  for (int s = 0; s < scaling; ++s)
+    for (int j = 1; j <= order && rc == LG_OK; ++j) {
+      A.first = s == 0 && j == 1;
+      A.last = j == order;
+      A.r = 1.0 / ((double)scaling * j);  // multiply by the reciprocal, src/expm.py:349
+      A.X = x;
+      A.T = outs[k];
+      void* args[] = {&A};
+      rc = launch(lg_ell_taylor_kernel(), grid, dim3(256), args, 0, st);
+      x = outs[k];
+      k ^= 1;
+    }
+  if (rc == LG_OK) {
+    cudaMemcpyAsync(out, cur, sizeof(double2) * h.size(), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(LG_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  cudaStreamDestroy(st);
+  return rc;
 }
 
 int lg_finalize_host(lg_problem* p, int64_t N, const double* raw, double* cost, double* grad) {

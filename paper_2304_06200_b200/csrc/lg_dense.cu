@@ -278,6 +278,41 @@ extern "C" __global__ void lg_k_axpy(const __grid_constant__ LgAxpyArgs A) {
   }
 }
 
+// One Taylor term of the standalone action exp(A) psi (src/expm.py:345-350) over ncol vectors
+// (column c at c * d): t = (A x) r;  cur = (first ? xin : cur) + t;  T = last ? cur : t.
+struct LgEllTaylorArgs {
+  int d, W, ncol, first, last;
+  double r;
+  const int* cols;
+  const double2* vals;
+  const double2* X;
+  const double2* xin;
+  double2* cur;
+  double2* T;
+};
+extern "C" __global__ void lg_k_ell_taylor(const __grid_constant__ LgEllTaylorArgs A) {
+  const int c = blockIdx.y;
+  const double2* x = A.X + (long)c * A.d;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.d; i += gridDim.x * blockDim.x) {
+    double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
+    for (int w = 0; w < A.W; ++w) {
+      const double2 a = A.vals[(long)w * A.d + i], b = x[A.cols[(long)w * A.d + i]];
+      p.x = fma(a.x, b.x, p.x);
+      p.y = fma(a.x, b.y, p.y);
+      q.x = fma(-a.y, b.y, q.x);
+      q.y = fma(a.y, b.x, q.y);
+    }
+    const double2 t = make_double2((p.x + q.x) * A.r, (p.y + q.y) * A.r);
+    const long o = (long)c * A.d + i;
+    double2 cu = A.first ? A.xin[o] : A.cur[o];
+    cu.x += t.x;
+    cu.y += t.y;
+    A.cur[o] = cu;
+    A.T[o] = A.last ? cu : t;
+  }
+}
+
+extern "C" void* lg_ell_taylor_kernel() { return (void*)lg_k_ell_taylor; }
 extern "C" void* lg_zgemm_kernel() { return (void*)lg_k_zgemm_taylor; }
 extern "C" void* lg_dense_form_kernel() { return (void*)lg_k_dense_form; }
 extern "C" void* lg_dots_kernel() { return (void*)lg_k_dots; }

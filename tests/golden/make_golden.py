@@ -427,7 +427,46 @@ def golden_full_basis_check():
          live_g1=r1.live_vector_peak)
 
 
+def golden_expm():
+    """Standalone certified action: reference expm.make_plan / expm.expm_multiply (src/expm.py:279-369)
+    on random anti-Hermitian CSR and dense generators, the sigma_x rotation, the zero generator and a
+    banded transmon-cavity generator; three states each (the reference takes one vector at a time)."""
+    rng = np.random.default_rng(4242)
+
+    def anti(d, scale):
+        g = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        return scale * (g - g.conj().T) / 2.0
+
+    h_s, hx, hy = tc_ops(6, 200)
+    hn = sparse.linear_combine([1.0, 0.01, -0.007], [h_s, hx, hy])
+    cases = {
+        "csr16": (sparse.from_dense(anti(16, 1.5)), (1e-8, 1e-12)),
+        "dense12": (sparse.DenseMatrix(np.asfortranarray(anti(12, 0.8))), (1e-10,)),
+        "rot": (sparse.build_csr([(0, 1, -1j * np.pi / 2), (1, 0, -1j * np.pi / 2)], 2, 2), (1e-10,)),
+        "zero": (sparse.build_csr([], 5, 5), (1e-8,)),
+        "band1200": (hn.scaled(-1j * 0.5), (1e-8,)),
+    }
+    out = {}
+    for tag, (a, taus) in cases.items():
+        d = a.n_rows
+        psi = rand_states(rng, 3, d)
+        out.update({f"{tag}__{k}": v for k, v in csr_arrays("a", a).items()})
+        out[f"{tag}__psi"] = psi
+        out[f"{tag}__norm1"] = np.float64(a.one_norm())
+        out[f"{tag}__sp"] = np.int64(a.max_row_nnz())
+        for i, tau in enumerate(taus):
+            plan = expm.make_plan(a.one_norm(), a.max_row_nnz(), tau)
+            res = [expm.expm_multiply(a, psi[h], tau) for h in range(3)]
+            out[f"{tag}__tau{i}"] = np.float64(tau)
+            out[f"{tag}__m{i}"] = np.int64(plan.order)
+            out[f"{tag}__s{i}"] = np.int64(plan.scaling)
+            out[f"{tag}__mu{i}"] = np.int64(res[0][1])
+            out[f"{tag}__out{i}"] = np.array([r[0] for r in res])
+    save("expm", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["planner", "numpy_rules", "full_basis_check", "c1", "c2", "stress", "c3", "c4", "c5"]
+    which = sys.argv[1:] or ["planner", "numpy_rules", "full_basis_check", "c1", "c2", "stress", "c3", "c4", "c5",
+                             "expm"]
     for w in which:
         globals()["golden_" + w]()
