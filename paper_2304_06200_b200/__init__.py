@@ -19,6 +19,7 @@ from .costs import (
     c3_gate_grad,
     c3_state_grad,
     composite_cost,
+    composite_cost_batch,
     composite_grad,
     forward_propagate,
 )
@@ -29,7 +30,7 @@ from .sparse import CsrMatrix, DenseMatrix, build_csr, build_csr_arrays, from_de
 __all__ = [
     "Backend", "ControlField", "ControlProblem", "CostKind", "CostTerm", "GradientResult",
     "c1_gate_grad", "c1_state_grad", "c2_state_grad", "c3_gate_grad", "c3_state_grad",
-    "composite_cost", "composite_grad", "forward_propagate", "ExpmPlan", "PlanningError", "make_plan",
+    "composite_cost", "composite_cost_batch", "composite_grad", "forward_propagate", "ExpmPlan", "PlanningError", "make_plan",
     "OptimizationTrace", "OptimizerConfig", "grape_optimize", "CsrMatrix", "DenseMatrix", "build_csr",
     "build_csr_arrays", "from_dense", "identity_csr", "linear_combine",
 ]

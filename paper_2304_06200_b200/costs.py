@@ -440,6 +440,37 @@ def composite_cost(problem: ControlProblem, a: ControlField, terms) -> float:
     return npb.cost(a)
 
 
+_POOLS: "OrderedDict[tuple, tuple]" = OrderedDict()
+
+
+def composite_cost_batch(problem: ControlProblem, fields, terms) -> list:
+    """``composite_cost`` for several fields at once (the line-search path,
+    src/optimizer.py:153-170).  Each field gets its own device problem and stream and the
+    evaluations run concurrently; every cost is bit-identical to ``composite_cost`` of that field."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    terms, has_state = _split(terms)
+    fields = list(fields)
+    for a in fields:
+        _check_field(problem, a)
+    if has_state and problem.initial_state is None:
+        raise ValueError("state-transfer terms require problem.initial_state")
+    if not fields:
+        return []
+    key = (id(problem), tuple(id(t) for t in terms))
+    hit = _POOLS.get(key)
+    pool = list(hit[0]) if hit else []
+    while len(pool) < len(fields):
+        pool.append(NativeProblem(problem, terms, problem.initial_state if has_state else None, problem.basis))
+    _POOLS[key] = (pool, problem, tuple(terms))
+    while len(_POOLS) > 4:
+        _POOLS.popitem(last=False)
+    if len(fields) == 1:
+        return [pool[0].cost(fields[0])]
+    with ThreadPoolExecutor(max_workers=len(fields)) as ex:
+        return list(ex.map(lambda pa: pa[0].cost(pa[1]), zip(pool, fields)))
+
+
 def _single(problem, a, psi0, term):
     _check_field(problem, a)
     npb = NativeProblem(problem, [term], initial_states=psi0)
