@@ -50,6 +50,7 @@ extern "C" void* lg_plans_kernel();
 extern "C" void* lg_gather_kernel();
 extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 extern "C" void* lg_zgemm_kernel();
+extern "C" void* lg_taylor_epi_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc);
 extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
@@ -79,6 +80,8 @@ struct LgGemmArgs {
   int ldt;
   double r;
   int first, last;
+  int ksplit;  // lg_dense.cu: split-k slices (partial products in `partial`)
+  double2* partial;
 };
 struct LgDotArgs {
   int d, n;
@@ -264,6 +267,8 @@ struct lg_problem {
   int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
   int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
   bool ws_cluster = false;
+  double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
+  size_t splitws_cap = 0;
   // cluster engine
   int cl_CS = 0, cl_R = 0, cl_H = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
@@ -327,6 +332,7 @@ struct lg_problem {
     nmem.release();
     dtmem.release();
     mem.release();
+    if (d_splitws) cudaFree(d_splitws);
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
   void mark(int i) {
@@ -679,8 +685,30 @@ int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2*
   G.r = r;
   G.first = first;
   G.last = last;
+  // split-k when the output tiles alone cannot fill the GPU (tall-skinny Taylor terms, 4 warps per
+  // 64 x 16 tile): deterministic, slices summed in order by lg_k_taylor_epi.  Measured at d = 4096:
+  // C = 64: 22.6 (1 slice) -> 29.7 TF/s (4); C = 128: 25.8 -> 31.2 TF/s (4) (tools/bench_zgemm.py).
+  const long nct = (long)((C + 15) / 16) * ((d + 63) / 64);
+  int ks = (int)std::max<long>(1, std::min<long>(4, 2048L / std::max<long>(nct, 1)));
+  if (const char* e = std::getenv("LG_SPLITK")) ks = std::max(1, std::atoi(e));
+  G.ksplit = ks;
+  if (ks > 1) {
+    const size_t need = (size_t)ks * d * C;
+    if (need > p->splitws_cap) {
+      if (p->d_splitws) cudaFree(p->d_splitws);
+      p->d_splitws = nullptr;
+      p->splitws_cap = 0;
+      if (cudaMalloc(&p->d_splitws, need * sizeof(double2)) != cudaSuccess) return fail(LG_CUDA_ERROR, "split-k workspace");
+      p->splitws_cap = need;
+    }
+    G.partial = p->d_splitws;
+  }
   void* args[] = {&G};
-  return launch(lg_zgemm_kernel(), dim3((C + 15) / 16, (d + 63) / 64), dim3(128), args, 0, p->stream);
+  int rc = launch(lg_zgemm_kernel(), dim3((C + 15) / 16, (d + 63) / 64, ks), dim3(128), args, 0, p->stream);
+  if (rc || ks == 1) return rc;
+  const long mc = (long)d * C;
+  return launch(lg_taylor_epi_kernel(), dim3((unsigned)std::min<long>((mc + 255) / 256, 148 * 8)), dim3(256), args, 0,
+                p->stream);
 }
 
 // cur <- (T_m(sgn A / s))^s x over C columns (columns contiguous, stride d)

@@ -54,9 +54,11 @@ struct LgGemmArgs {
   int ldt;
   double r;
   int first, last;
+  int ksplit;        // > 1: grid.z slices the k-tiles; each slice writes its raw product to
+  double2* partial;  //     partial[z][n * M + m] and lg_k_taylor_epi finishes the term
 };
 
-// grid (ceil(C / BN), ceil(M / BM)); 128 threads = 4 warps, each a 16 x 16 tile.
+// grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x 16 tile.
 extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
   __shared__ __align__(16) double sAr[2][BK][SA];
   __shared__ __align__(16) double sAi[2][BK][SA];
@@ -71,12 +73,16 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
     for (int b = 0; b < 2; ++b) yr[a][b][0] = yr[a][b][1] = yi[a][b][0] = yi[a][b][1] = 0.0;
 
-  // flattened k-tiles over the segments
+  // flattened k-tiles over the segments; this CTA's slice [t_lo, t_hi)
   int tiles0 = (G.seg[0].K + BK - 1) / BK;
-  int total = tiles0 + (G.nseg > 1 ? (G.seg[1].K + BK - 1) / BK : 0);
+  const int all_tiles = tiles0 + (G.nseg > 1 ? (G.seg[1].K + BK - 1) / BK : 0);
+  const int t_lo = (int)((long)all_tiles * blockIdx.z / gridDim.z);
+  const int t_hi = (int)((long)all_tiles * (blockIdx.z + 1) / gridDim.z);
+  const int total = t_hi - t_lo;
   const bool full_m = (m0 + BM <= M);
 
-  auto load_tile = [&](int t, int buf, double2* xreg) {
+  auto load_tile = [&](int tl, int buf, double2* xreg) {
+    const int t = t_lo + tl;
     const LgGemmSeg& S = G.seg[t < tiles0 ? 0 : 1];
     const int k0 = (t < tiles0 ? t : t - tiles0) * BK;
     // A: BK columns x BM rows per plane; 16-byte chunks: BK * BM / 2 per plane
@@ -143,13 +149,20 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
         xi[nt] = sXi[buf][ka][n];
         nxi[nt] = -xi[nt];
       }
+      // all Ar products first, then all Ai products: 8 independent DMMAs separate the two
+      // updates of an accumulator (back-to-back they stall on the DMMA latency)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           dmma(yr[mt][nt][0], yr[mt][nt][1], ar[mt], xr[nt]);
-          dmma(yr[mt][nt][0], yr[mt][nt][1], ai[mt], nxi[nt]);
           dmma(yi[mt][nt][0], yi[mt][nt][1], ar[mt], xi[nt]);
+        }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(yr[mt][nt][0], yr[mt][nt][1], ai[mt], nxi[nt]);
           dmma(yi[mt][nt][0], yi[mt][nt][1], ai[mt], xr[nt]);
         }
     }
@@ -157,6 +170,20 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
       __syncthreads();  // everyone done reading sX[buf ^ 1] of tile t - 1
       store_x(buf ^ 1, xreg);
     }
+  }
+  if (G.ksplit > 1) {  // raw partial product of this k-slice
+    double2* P = G.partial + (long)blockIdx.z * M * C;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
+          const int n = n0 + nt * 8 + 2 * (lane & 3) + v;
+          if (m < M && n < C) P[(long)n * M + m] = make_double2(yr[mt][nt][v], yi[mt][nt][v]);
+        }
+    return;
   }
   // fused Taylor epilogue
   const double r = G.r;
@@ -179,6 +206,29 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
         G.cur[(long)n * G.ldc + m] = cu;
         G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
       }
+}
+
+// Split-k finish: y = sum of the k-slices in slice order (deterministic), then the Taylor update.
+extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G) {
+  const long MC = (long)G.M * G.C;
+  for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < MC; q += (long)gridDim.x * blockDim.x) {
+    double2 y = G.partial[q];
+    for (int z = 1; z < G.ksplit; ++z) {
+      const double2 pz = G.partial[(long)z * MC + q];
+      y.x += pz.x;
+      y.y += pz.y;
+    }
+    const int m = (int)(q % G.M), n = (int)(q / G.M);
+    const double2 tt = make_double2(y.x * G.r, y.y * G.r);
+    double2 base;
+    if (G.first)
+      base = G.xin ? G.xin[(long)n * G.ldxin + m] : make_double2(0.0, 0.0);
+    else
+      base = G.cur[(long)n * G.ldc + m];
+    const double2 cu = make_double2(base.x + tt.x, base.y + tt.y);
+    G.cur[(long)n * G.ldc + m] = cu;
+    G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
+  }
 }
 
 // A_n = -i dt (H_s + sum_c a_c h_c), planar column-major, same operand order as
@@ -314,6 +364,7 @@ extern "C" __global__ void lg_k_ell_taylor(const __grid_constant__ LgEllTaylorAr
 
 extern "C" void* lg_ell_taylor_kernel() { return (void*)lg_k_ell_taylor; }
 extern "C" void* lg_zgemm_kernel() { return (void*)lg_k_zgemm_taylor; }
+extern "C" void* lg_taylor_epi_kernel() { return (void*)lg_k_taylor_epi; }
 extern "C" void* lg_dense_form_kernel() { return (void*)lg_k_dense_form; }
 extern "C" void* lg_dots_kernel() { return (void*)lg_k_dots; }
 extern "C" void* lg_ell_kernel() { return (void*)lg_k_ell_apply; }
