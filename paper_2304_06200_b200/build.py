@@ -25,6 +25,9 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "
 UNITS = {
     "lg_prep.cu": ["-fmad=false"],
     "lg_api.cu": ["-fmad=false"],
+    "lg_host.cu": ["-fmad=false"],
+    "lg_configure.cu": ["-fmad=false"],
+    "lg_dense_host.cu": ["-fmad=false"],
     "lg_engine.cu": [],
     "lg_sweep_cta.cu": ["-DLG_DEBUG"] if os.environ.get("LG_DEBUG") else [],
     "lg_dense.cu": [],

@@ -33,30 +33,7 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 }  // namespace
 
-struct LgGemmSeg {
-  const double* Ar;  // column-major, element (i, k) at k * lda + i
-  const double* Ai;
-  int lda;
-  const double2* X;  // column-major, element (k, c) at c * ldx + k
-  int ldx;
-  int K;
-};
 
-struct LgGemmArgs {
-  int M, C;
-  LgGemmSeg seg[2];
-  int nseg;
-  const double2* xin;  // cur initialisation on the first term (nullptr: zero)
-  int ldxin;
-  double2* cur;
-  int ldc;
-  double2* tout;
-  int ldt;
-  double r;
-  int first, last;
-  int ksplit;        // > 1: grid.z slices the k-tiles; each slice writes its raw product to
-  double2* partial;  //     partial[z][n * M + m] and lg_k_taylor_epi finishes the term
-};
 
 // grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x 16 tile.
 extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
@@ -249,15 +226,6 @@ extern "C" __global__ void lg_k_dense_form(const double2* hs, const double2* con
   }
 }
 
-// Deterministic dot products <u_p | v_p> = sum_i conj(u_p[i]) v_p[i] for a list of
-// column pairs (one CTA per pair, fixed-order tree).  mode bit0: conjugate-free
-// variant not needed; out[p] written.
-struct LgDotArgs {
-  int d, n;
-  const double2* u[64];
-  const double2* v[64];
-  double2* out[64];
-};
 extern "C" __global__ void lg_k_dots(const __grid_constant__ LgDotArgs D) {
   __shared__ double2 red[32];
   const int p = blockIdx.x;
@@ -283,14 +251,6 @@ extern "C" __global__ void lg_k_dots(const __grid_constant__ LgDotArgs D) {
   }
 }
 
-// y[c] = O x[c] for an ELL operator over several columns; optionally y += (mode 1)
-struct LgEllArgs {
-  int d, W, ncol, accumulate;
-  const int* cols;
-  const double2* vals;
-  const double2* x[64];
-  double2* y[64];
-};
 extern "C" __global__ void lg_k_ell_apply(const __grid_constant__ LgEllArgs A) {
   const int c = blockIdx.y;
   const double2* x = A.x[c];
@@ -306,15 +266,6 @@ extern "C" __global__ void lg_k_ell_apply(const __grid_constant__ LgEllArgs A) {
   }
 }
 
-// y[c] = alpha_c * u[c] (+ y[c] when accumulate): costate initialisation / sources.
-struct LgAxpyArgs {
-  int d, ncol;
-  const double2* u[64];
-  double2* y[64];
-  double2 alpha[64];
-  const double2* alpha_ptr[64];  // optional device scalar multiplier (nullptr: use alpha)
-  int accumulate[64];
-};
 extern "C" __global__ void lg_k_axpy(const __grid_constant__ LgAxpyArgs A) {
   const int c = blockIdx.y;
   const double2* u = A.u[c];
@@ -328,18 +279,6 @@ extern "C" __global__ void lg_k_axpy(const __grid_constant__ LgAxpyArgs A) {
   }
 }
 
-// One Taylor term of the standalone action exp(A) psi (src/expm.py:345-350) over ncol vectors
-// (column c at c * d): t = (A x) r;  cur = (first ? xin : cur) + t;  T = last ? cur : t.
-struct LgEllTaylorArgs {
-  int d, W, ncol, first, last;
-  double r;
-  const int* cols;
-  const double2* vals;
-  const double2* X;
-  const double2* xin;
-  double2* cur;
-  double2* T;
-};
 extern "C" __global__ void lg_k_ell_taylor(const __grid_constant__ LgEllTaylorArgs A) {
   const int c = blockIdx.y;
   const double2* x = A.X + (long)c * A.d;

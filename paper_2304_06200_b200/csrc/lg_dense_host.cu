@@ -1,0 +1,442 @@
+// Host units, part 3: the dense (DMMA) engine driver -- per-step host loop over the dense Taylor
+// GEMMs (lg_dense.cu), derivative chains, costate sources and per-step scalars.
+#include "lg_host.h"
+
+namespace lgi {
+
+int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2* X, const double* Br,
+               const double* Bi, const double2* Xb, int C, double r, bool first, bool last, const double2* xin,
+               double2* cur, double2* tout) {
+  LgGemmArgs G{};
+  const int d = (int)p->d;
+  G.M = d;
+  G.C = C;
+  G.seg[0] = LgGemmSeg{Ar, Ai, d, X, d, d};
+  G.nseg = 1;
+  if (Br) {
+    G.seg[1] = LgGemmSeg{Br, Bi, d, Xb, d, d};
+    G.nseg = 2;
+  }
+  G.xin = xin;
+  G.ldxin = d;
+  G.cur = cur;
+  G.ldc = d;
+  G.tout = tout;
+  G.ldt = d;
+  G.r = r;
+  G.first = first;
+  G.last = last;
+  // split-k when the output tiles alone cannot fill the GPU (tall-skinny Taylor terms, 4 warps per
+  // 64 x 16 tile): deterministic, slices summed in order by lg_k_taylor_epi.  Measured at d = 4096:
+  // C = 64: 22.6 (1 slice) -> 29.7 TF/s (4); C = 128: 25.8 -> 31.2 TF/s (4) (tools/bench_zgemm.py).
+  const long nct = (long)((C + 15) / 16) * ((d + 63) / 64);
+  int ks = (int)std::max<long>(1, std::min<long>(4, 2048L / std::max<long>(nct, 1)));
+  if (const char* e = std::getenv("LG_SPLITK")) ks = std::max(1, std::atoi(e));
+  G.ksplit = ks;
+  if (ks > 1) {
+    const size_t need = (size_t)ks * d * C;
+    if (need > p->splitws_cap) {
+      if (p->d_splitws) cudaFree(p->d_splitws);
+      p->d_splitws = nullptr;
+      p->splitws_cap = 0;
+      if (cudaMalloc(&p->d_splitws, need * sizeof(double2)) != cudaSuccess) return fail(LG_CUDA_ERROR, "split-k workspace");
+      p->splitws_cap = need;
+    }
+    G.partial = p->d_splitws;
+  }
+  void* args[] = {&G};
+  int rc = launch(lg_zgemm_kernel(), dim3((C + 15) / 16, (d + 63) / 64, ks), dim3(128), args, 0, p->stream);
+  if (rc || ks == 1) return rc;
+  const long mc = (long)d * C;
+  return launch(lg_taylor_epi_kernel(), dim3((unsigned)std::min<long>((mc + 255) / 256, 148 * 8)), dim3(256), args, 0,
+                p->stream);
+}
+
+// cur <- (T_m(sgn A / s))^s x over C columns (columns contiguous, stride d)
+int dense_chain(lg_problem* p, int C, double sgn, int m, int s, const double2* x, double2* cur) {
+  const double2* prev = x;
+  double2* bufs[2] = {p->dd_tb0, p->dd_tb1};
+  int b = 0;
+  for (int si = 0; si < s; ++si)
+    for (int j = 1; j <= m; ++j) {
+      const bool first = si == 0 && j == 1;
+      int rc = dense_gemm(p, p->d_Ar, p->d_Ai, prev, nullptr, nullptr, nullptr, C, sgn * (1.0 / (double)(s * j)),
+                          first, j == m, first ? x : nullptr, cur, bufs[b]);
+      if (rc) return rc;
+      prev = bufs[b];
+      b ^= 1;
+    }
+  return LG_OK;
+}
+
+// aux embedding chain for channels gch[0..G): tops (G*T columns) then bottoms (T columns)
+int dense_aux_chain(lg_problem* p, int T, const int* gch, int G, int m, int s, const double2* psi) {
+  const long d = p->d;
+  double2* bufs[2] = {p->dd_xtb0, p->dd_xtb1};
+  const double2* prev = nullptr;
+  int b = 0;
+  for (int si = 0; si < s; ++si)
+    for (int j = 1; j <= m; ++j) {
+      const bool first = si == 0 && j == 1, last = j == m;
+      const double r = 1.0 / (double)(s * j);
+      double2* out = bufs[b];
+      for (int gi = 0; gi < G; ++gi) {
+        const int k = gch[gi];
+        int rc;
+        if (first)
+          rc = dense_gemm(p, p->d_Acr[k], p->d_Aci[k], psi, nullptr, nullptr, nullptr, T, r, true, last, nullptr,
+                          p->dd_xcur + gi * T * d, out + gi * T * d);
+        else
+          rc = dense_gemm(p, p->d_Ar, p->d_Ai, prev + gi * T * d, p->d_Acr[k], p->d_Aci[k], prev + (long)G * T * d, T,
+                          r, false, last, nullptr, p->dd_xcur + gi * T * d, out + gi * T * d);
+        if (rc) return rc;
+      }
+      int rc = dense_gemm(p, p->d_Ar, p->d_Ai, first ? psi : prev + (long)G * T * d, nullptr, nullptr, nullptr, T, r,
+                          first, last, first ? psi : nullptr, p->dd_xcur + (long)G * T * d, out + (long)G * T * d);
+      if (rc) return rc;
+      prev = out;
+      b ^= 1;
+    }
+  return LG_OK;
+}
+
+int dense_form(lg_problem* p, const double2* hs, double2** hc_dev, const double* amps, int kc, double dt, double* Ar,
+               double* Ai) {
+  long count = p->d * p->d;
+  void* args[] = {&hs, &hc_dev, &amps, &kc, &dt, &count, &Ar, &Ai};
+  return launch(lg_dense_form_kernel(), dim3(148 * 8), dim3(256), args, 0, p->stream);
+}
+
+// deterministic dots over pairs; results copied to host
+int dense_dots(lg_problem* p, const std::vector<std::pair<const double2*, const double2*>>& pr, std::vector<double2>& out) {
+  out.assign(pr.size(), make_double2(0.0, 0.0));
+  for (size_t b0 = 0; b0 < pr.size(); b0 += 64) {
+    LgDotArgs D{};
+    D.d = (int)p->d;
+    D.n = (int)std::min<size_t>(64, pr.size() - b0);
+    for (int q = 0; q < D.n; ++q) {
+      D.u[q] = pr[b0 + q].first;
+      D.v[q] = pr[b0 + q].second;
+      D.out[q] = p->dd_dots + b0 + q;
+    }
+    void* args[] = {&D};
+    int rc = launch(lg_dots_kernel(), dim3(D.n), dim3(256), args, 0, p->stream);
+    if (rc) return rc;
+  }
+  if (!pr.empty()) {
+    CK(cudaMemcpyAsync(out.data(), p->dd_dots, sizeof(double2) * pr.size(), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
+  return LG_OK;
+}
+
+int dense_ell(lg_problem* p, const Spec& sp, const std::vector<const double2*>& x, const std::vector<double2*>& y,
+              bool acc) {
+  for (size_t b0 = 0; b0 < x.size(); b0 += 64) {
+    LgEllArgs A{};
+    A.d = (int)p->d;
+    A.W = sp.pen_W;
+    A.ncol = (int)std::min<size_t>(64, x.size() - b0);
+    A.accumulate = acc;
+    A.cols = sp.d_pen_cols;
+    A.vals = sp.d_pen_vals;
+    for (int q = 0; q < A.ncol; ++q) {
+      A.x[q] = x[b0 + q];
+      A.y[q] = y[b0 + q];
+    }
+    void* args[] = {&A};
+    int rc = launch(lg_ell_kernel(), dim3((unsigned)((p->d + 255) / 256), A.ncol), dim3(256), args, 0, p->stream);
+    if (rc) return rc;
+  }
+  return LG_OK;
+}
+
+int dense_axpy(lg_problem* p, const std::vector<const double2*>& u, const std::vector<double2*>& y,
+               const std::vector<double2>& alpha, bool acc) {
+  for (size_t b0 = 0; b0 < u.size(); b0 += 64) {
+    LgAxpyArgs A{};
+    A.d = (int)p->d;
+    A.ncol = (int)std::min<size_t>(64, u.size() - b0);
+    for (int q = 0; q < A.ncol; ++q) {
+      A.u[q] = u[b0 + q];
+      A.y[q] = y[b0 + q];
+      A.alpha[q] = alpha[b0 + q];
+      A.alpha_ptr[q] = nullptr;
+      A.accumulate[q] = acc;
+    }
+    void* args[] = {&A};
+    int rc = launch(lg_axpy_kernel(), dim3((unsigned)((p->d + 255) / 256), A.ncol), dim3(256), args, 0, p->stream);
+    if (rc) return rc;
+  }
+  return LG_OK;
+}
+
+int configure_dense(lg_problem* p) {
+  const long d = p->d;
+  int nspec[2] = {0, 0};
+  for (auto& s : p->specs) nspec[s.set]++;
+  const int Imax = std::max({1, nspec[0], nspec[1]});
+  int Tmax = 1;
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    Tmax = std::max(Tmax, hi - lo);
+  }
+  const long cst = (long)Tmax * (1 + Imax), cx = (long)(p->Kc + 1) * Tmax;
+  DevMem& M = p->mem;
+  p->d_Ar = M.alloc<double>((size_t)d * d);
+  p->d_Ai = M.alloc<double>((size_t)d * d);
+  p->d_Acr.assign(p->Kc, nullptr);
+  p->d_Aci.assign(p->Kc, nullptr);
+  for (int c = 0; c < p->Kc; ++c) {
+    p->d_Acr[c] = M.alloc<double>((size_t)d * d);
+    p->d_Aci[c] = M.alloc<double>((size_t)d * d);
+  }
+  p->dd_st = M.alloc<double2>((size_t)cst * d);
+  p->dd_nx = M.alloc<double2>((size_t)cst * d);
+  p->dd_cur = M.alloc<double2>((size_t)cst * d);
+  p->dd_tb0 = M.alloc<double2>((size_t)cst * d);
+  p->dd_tb1 = M.alloc<double2>((size_t)cst * d);
+  p->dd_xcur = M.alloc<double2>((size_t)cx * d);
+  p->dd_xtb0 = M.alloc<double2>((size_t)cx * d);
+  p->dd_xtb1 = M.alloc<double2>((size_t)cx * d);
+  p->dd_tmp = M.alloc<double2>((size_t)Tmax * d);
+  p->dd_dots = M.alloc<double2>((size_t)std::max<long>(64, (long)Imax * p->Kc * Tmax + 2 * cst));
+  if (!p->dd_dots || !p->dd_xtb1 || !p->d_Ai) return fail(LG_CUDA_ERROR, "device allocation failed (dense engine)");
+  p->engine = 3;
+  p->n_groups = 0;
+  p->live_peak = (int)((3 * cst + 3 * cx + Tmax - 1) / Tmax);
+  p->d_bar = M.alloc<unsigned>(4);
+  p->d_scratch = M.alloc<double2>(1);
+  p->d_red = M.alloc<double2>(1);
+  return LG_OK;
+}
+
+int run_dense(lg_problem* p, long N, double dt, bool grad) {
+  const long d = p->d;
+  const int Kc = p->Kc, S = (int)p->specs.size(), Tt = p->T_total;
+  int rc;
+  std::vector<int4> pl((size_t)N * (Kc + 1));
+  CK(cudaMemcpyAsync(pl.data(), p->d_plan, sizeof(int4) * pl.size(), cudaMemcpyDeviceToHost, p->stream));
+  std::vector<double> amps((size_t)N * Kc);
+  CK(cudaMemcpyAsync(amps.data(), p->d_amps, sizeof(double) * amps.size(), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (!(p->dense_dt == dt)) {
+    for (int c = 0; c < Kc; ++c) {
+      double2** none = nullptr;
+      rc = dense_form(p, p->d_hc_dense_host[c], none, nullptr, 0, dt, p->d_Acr[c], p->d_Aci[c]);
+      if (rc) return rc;
+    }
+    p->dense_dt = dt;
+  }
+  std::vector<double2> ip((size_t)N * std::max(S, 1) * Kc * std::max(Tt, 1), make_double2(0, 0)),
+      fin((size_t)std::max(S, 1) * std::max(Tt, 1), make_double2(0, 0)),
+      trp((size_t)std::max(S, 1) * N * std::max(Tt, 1), make_double2(0, 0));
+  std::vector<double> run((size_t)std::max(S, 1) * std::max(Tt, 1), 0.0);
+  std::vector<double2> dots;
+  // sharded running gate costs: every rank all-reduces the set's traces between its sweeps
+  auto trace_hook = [&](int set) -> int {
+    if (!grad || !p->hook) return LG_OK;
+    bool any = false;
+    for (int s = 0; s < S; ++s) any |= p->specs[s].set == set && p->specs[s].kind == LGK_GATE_RUN;
+    if (!any) return LG_OK;
+    CK(cudaMemcpyAsync(p->d_trp, trp.data(), sizeof(double2) * trp.size(), cudaMemcpyHostToDevice, p->stream));
+    if (p->hook(reinterpret_cast<double*>(p->d_trp), 2 * (long)trp.size(), p->stream, p->hook_user) != 0)
+      return fail(LG_CUDA_ERROR, "all-reduce hook failed (traces)");
+    CK(cudaMemcpyAsync(trp.data(), p->d_trp, sizeof(double2) * trp.size(), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    p->trp_reduced = true;
+    return LG_OK;
+  };
+  for (int set = 0; set < 2; ++set) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[set]), hi = (int)std::min<long>(p->shard_e, p->set_T[set]);
+    const int T = hi - lo;
+    if (T <= 0) {
+      if (int rh = trace_hook(set)) return rh;
+      continue;
+    }
+    const int t0 = p->set_t0[set] + lo;  // global trajectory index of column 0
+    std::vector<int> sp_idx;
+    for (int s = 0; s < S; ++s)
+      if (p->specs[s].set == set) sp_idx.push_back(s);
+    const int I = (int)sp_idx.size();
+    auto col = [&](double2* base, int c) { return base + (long)c * d; };
+    auto tgt = [&](int s, int t) { return p->specs[s].d_tgt + (long)(lo + t) * d; };
+    CK(cudaMemcpyAsync(p->dd_st, p->d_traj + (long)t0 * d, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
+    // ---- forward sweep
+    for (long n = 0; n < N; ++n) {
+      const int4 q = pl[(size_t)n * (Kc + 1)];
+      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ar, p->d_Ai);
+      if (rc) return rc;
+      rc = dense_chain(p, T, 1.0, q.x, q.y, p->dd_st, p->dd_cur);
+      if (rc) return rc;
+      CK(cudaMemcpyAsync(p->dd_st, p->dd_cur, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
+      const bool fin_step = n == N - 1;
+      std::vector<std::pair<const double2*, const double2*>> pr;
+      std::vector<std::pair<int, int>> who;  // (spec, t)
+      for (int s : sp_idx) {
+        const int kind = p->specs[s].kind;
+        if (kind == LGK_STATE_PEN) {
+          std::vector<const double2*> x;
+          std::vector<double2*> y;
+          for (int t = 0; t < T; ++t) x.push_back(col(p->dd_st, t)), y.push_back(col(p->dd_tmp, t));
+          rc = dense_ell(p, p->specs[s], x, y, false);
+          if (rc) return rc;
+          for (int t = 0; t < T; ++t) pr.push_back({col(p->dd_st, t), col(p->dd_tmp, t)}), who.push_back({s, t});
+        } else if (kind == LGK_STATE_RUN || kind == LGK_GATE_RUN || (fin_step && kind == LGK_GATE)) {
+          for (int t = 0; t < T; ++t) pr.push_back({tgt(s, t), col(p->dd_st, t)}), who.push_back({s, t});
+        } else if (fin_step && kind == LGK_STATE_INF) {
+          for (int t = 0; t < T; ++t) pr.push_back({col(p->dd_st, t), tgt(s, t)}), who.push_back({s, t});
+        }
+        if (kind == LGK_STATE_PEN && !pr.empty()) {
+          // penalty dots must be taken before tmp is reused by another penalty term
+          rc = dense_dots(p, pr, dots);
+          if (rc) return rc;
+          for (size_t z = 0; z < pr.size(); ++z) {
+            const int s2 = who[z].first, t = who[z].second;
+            const long o = (long)s2 * Tt + t0 + t;
+            const int k2 = p->specs[s2].kind;
+            if (k2 == LGK_STATE_PEN) run[o] += dots[z].x;
+            else if (k2 == LGK_STATE_RUN) { const double a = std::hypot(dots[z].x, dots[z].y); run[o] += a * a; }
+            else if (k2 == LGK_GATE_RUN) trp[((long)s2 * N + n) * Tt + t0 + t] = dots[z];
+            else fin[o] = dots[z];
+          }
+          pr.clear();
+          who.clear();
+        }
+      }
+      rc = dense_dots(p, pr, dots);
+      if (rc) return rc;
+      for (size_t z = 0; z < pr.size(); ++z) {
+        const int s2 = who[z].first, t = who[z].second;
+        const long o = (long)s2 * Tt + t0 + t;
+        const int k2 = p->specs[s2].kind;
+        if (k2 == LGK_STATE_PEN) run[o] += dots[z].x;
+        else if (k2 == LGK_STATE_RUN) { const double a = std::hypot(dots[z].x, dots[z].y); run[o] += a * a; }
+        else if (k2 == LGK_GATE_RUN) trp[((long)s2 * N + n) * Tt + t0 + t] = dots[z];
+        else fin[o] = dots[z];
+      }
+    }
+    CK(cudaMemcpyAsync(p->d_psiN + (long)t0 * d, p->dd_st, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
+    if (int rh = trace_hook(set)) return rh;
+    if (!grad || I == 0) continue;
+    // running gate traces summed over the set (trajectory order)
+    std::vector<double2> trsum((size_t)S * N, make_double2(0, 0));
+    for (int s : sp_idx)
+      if (p->specs[s].kind == LGK_GATE_RUN)
+        for (long n = 0; n < N; ++n)
+          for (int t = 0; t < p->set_T[set]; ++t) {
+            const double2 v = trp[((long)s * N + n) * Tt + p->set_t0[set] + t];
+            trsum[(size_t)s * N + n].x += v.x;
+            trsum[(size_t)s * N + n].y += v.y;
+          }
+    auto lam = [&](double2* base, int si, int t) { return col(base, T + si * T + t); };
+    // ---- costate initialisation (src/costs.py:312-321, :457-460)
+    {
+      std::vector<std::pair<const double2*, const double2*>> pr;
+      for (int si = 0; si < I; ++si)
+        if (p->specs[sp_idx[si]].kind == LGK_STATE_RUN)
+          for (int t = 0; t < T; ++t) pr.push_back({tgt(sp_idx[si], t), col(p->dd_st, t)});
+      rc = dense_dots(p, pr, dots);
+      if (rc) return rc;
+      size_t z = 0;
+      for (int si = 0; si < I; ++si) {
+        const int s = sp_idx[si];
+        const Spec& sp = p->specs[s];
+        std::vector<const double2*> u;
+        std::vector<double2*> y;
+        std::vector<double2> al;
+        for (int t = 0; t < T; ++t) {
+          if (sp.kind == LGK_STATE_PEN) continue;
+          u.push_back(tgt(s, t));
+          y.push_back(lam(p->dd_st, si, t));
+          if (sp.kind == LGK_STATE_RUN) al.push_back(dots[z++]);
+          else if (sp.kind == LGK_GATE_RUN) al.push_back(trsum[(size_t)s * N + N - 1]);
+          else al.push_back(make_double2(1.0, 0.0));
+        }
+        if (sp.kind == LGK_STATE_PEN) {
+          std::vector<const double2*> x;
+          std::vector<double2*> yy;
+          for (int t = 0; t < T; ++t) x.push_back(col(p->dd_st, t)), yy.push_back(lam(p->dd_st, si, t));
+          rc = dense_ell(p, sp, x, yy, false);
+        } else {
+          rc = dense_axpy(p, u, y, al, false);
+        }
+        if (rc) return rc;
+      }
+    }
+    // ---- backward sweep
+    int gch[LG_MAX_CHANNELS];
+    for (long n = N - 1; n >= 0; --n) {
+      const int4* pn = &pl[(size_t)n * (Kc + 1)];
+      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ar, p->d_Ai);
+      if (rc) return rc;
+      const int cadj = n > 0 ? T * (1 + I) : T;
+      rc = dense_chain(p, cadj, -1.0, pn[0].x, pn[0].y, p->dd_st, p->dd_nx);
+      if (rc) return rc;
+      unsigned done = 0;
+      for (int kc = 0; kc < Kc; ++kc) {
+        if (done & (1u << kc)) continue;
+        int G = 0;
+        for (int k2 = kc; k2 < Kc; ++k2)
+          if (!(done & (1u << k2)) && pn[1 + k2].x == pn[1 + kc].x && pn[1 + k2].y == pn[1 + kc].y) {
+            gch[G++] = k2;
+            done |= 1u << k2;
+          }
+        rc = dense_aux_chain(p, T, gch, G, pn[1 + kc].x, pn[1 + kc].y, p->dd_nx);
+        if (rc) return rc;
+        std::vector<std::pair<const double2*, const double2*>> pr;
+        for (int gi = 0; gi < G; ++gi)
+          for (int si = 0; si < I; ++si)
+            for (int t = 0; t < T; ++t) pr.push_back({lam(p->dd_st, si, t), p->dd_xcur + ((long)gi * T + t) * d});
+        rc = dense_dots(p, pr, dots);
+        if (rc) return rc;
+        size_t z = 0;
+        for (int gi = 0; gi < G; ++gi)
+          for (int si = 0; si < I; ++si)
+            for (int t = 0; t < T; ++t)
+              ip[(((size_t)n * S + sp_idx[si]) * Kc + gch[gi]) * Tt + t0 + t] = dots[z++];
+      }
+      if (n == 0) break;
+      // costate sources at psi_{n-1} (src/costs.py:341-353, :474-479)
+      std::vector<std::pair<const double2*, const double2*>> pr;
+      for (int si = 0; si < I; ++si)
+        if (p->specs[sp_idx[si]].kind == LGK_STATE_RUN)
+          for (int t = 0; t < T; ++t) pr.push_back({tgt(sp_idx[si], t), col(p->dd_nx, t)});
+      rc = dense_dots(p, pr, dots);
+      if (rc) return rc;
+      size_t z = 0;
+      for (int si = 0; si < I; ++si) {
+        const int s = sp_idx[si];
+        const Spec& sp = p->specs[s];
+        if (sp.kind == LGK_STATE_PEN) {
+          std::vector<const double2*> x;
+          std::vector<double2*> yy;
+          for (int t = 0; t < T; ++t) x.push_back(col(p->dd_nx, t)), yy.push_back(lam(p->dd_nx, si, t));
+          rc = dense_ell(p, sp, x, yy, true);
+        } else if (sp.kind == LGK_STATE_RUN || sp.kind == LGK_GATE_RUN) {
+          std::vector<const double2*> u;
+          std::vector<double2*> y;
+          std::vector<double2> al;
+          for (int t = 0; t < T; ++t) {
+            u.push_back(tgt(s, t));
+            y.push_back(lam(p->dd_nx, si, t));
+            al.push_back(sp.kind == LGK_STATE_RUN ? dots[z++] : trsum[(size_t)s * N + n - 1]);
+          }
+          rc = dense_axpy(p, u, y, al, true);
+        } else {
+          rc = LG_OK;
+        }
+        if (rc) return rc;
+      }
+      CK(cudaMemcpyAsync(p->dd_st, p->dd_nx, sizeof(double2) * T * (1 + I) * d, cudaMemcpyDeviceToDevice, p->stream));
+    }
+  }
+  CK(cudaMemcpyAsync(p->d_ip, ip.data(), sizeof(double2) * ip.size(), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->d_fin, fin.data(), sizeof(double2) * fin.size(), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->d_trp, trp.data(), sizeof(double2) * trp.size(), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->d_run, run.data(), sizeof(double) * run.size(), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return LG_OK;
+}
+
+}  // namespace lgi

@@ -1,0 +1,254 @@
+// Internal host-side declarations shared by the library's host units (lg_host.cu,
+// lg_configure.cu, lg_dense_host.cu, lg_api.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/leangrape_b200.h"
+#include "lg_final.cuh"
+#include "lg_numpy.cuh"
+#include "lg_planner.cuh"
+#include "lg_types.h"
+
+// kernel getters of the device units
+extern "C" void* lg_forward_kernel(int multi);
+extern "C" void* lg_backward_kernel(int multi);
+extern "C" void* lg_trsum_kernel();
+extern "C" void* lg_ell_taylor_kernel();
+extern "C" void* lg_finalize_kernel();
+extern "C" void* lg_prep_sparse_kernel();
+extern "C" void* lg_prep_dense_kernel();
+extern "C" void* lg_plans_kernel();
+extern "C" void* lg_gather_kernel();
+extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
+extern "C" void* lg_zgemm_kernel();
+extern "C" void* lg_taylor_epi_kernel();
+extern "C" void* lg_cl_kernel(int backward, int W, int maxc);
+extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw);
+extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
+extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp);
+extern "C" void* lg_dense_form_kernel();
+extern "C" void* lg_dots_kernel();
+extern "C" void* lg_ell_kernel();
+extern "C" void* lg_axpy_kernel();
+
+namespace lgi {
+
+extern thread_local std::string g_err;
+int fail(int code, const std::string& msg);
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(LG_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Mat {
+  bool dense = false;
+  long n = 0;
+  std::vector<long> indptr, indices;  // CSR
+  std::vector<double2> vals;          // CSR values or dense column-major
+  long nnz() const { return dense ? n * n : (long)indices.size(); }
+};
+
+int parse_mat(const lg_matrix& m, long d, Mat* out, const char* what);
+// ELL of one operator (for the engine): W = widest row, padded with (col = row, value 0).
+void to_ell(const Mat& m, int* W_out, std::vector<int>& cols, std::vector<double2>& vals, std::vector<int>* rowlen);
+
+inline double2 gen_host(double2 h, double dt) { return make_double2(dt * h.y, -(dt * h.x)); }
+
+struct DevMem {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (p && !v.empty()) cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+struct Spec {
+  int kind;
+  double weight;
+  int set;
+  std::vector<double2> tgt;  // [K_set][d]
+  Mat pen;
+  int pen_W = 0;
+  int* d_pen_cols = nullptr;
+  double2* d_pen_vals = nullptr;
+  double2* d_tgt = nullptr;
+};
+
+}  // namespace lgi
+
+using lgi::DevMem;
+using lgi::Mat;
+using lgi::Spec;
+
+struct lg_problem {
+  int device = 0;
+  long d = 0;
+  int Kc = 0;
+  bool dense = false, materialise = false;
+  double tau = 1e-8;
+  Mat hs;
+  std::vector<Mat> hc;
+  std::vector<Spec> specs;
+  // trajectories
+  int set_t0[2] = {0, 0}, set_T[2] = {0, 0};
+  int T_total = 0;
+  std::vector<double2> traj;
+  // union ELL
+  int W = 0;
+  std::vector<int> rowlen, cols, src_s, src_c, colptr, colent;
+  // control ELL
+  int Wc = 0;
+  std::vector<int> ccols, crowlen;
+  std::vector<double2> cvals;
+  // engine configuration
+  bool multi = false;
+  int engine = 0;  // 0 legacy single-CTA, 1 legacy multi-CTA (grid barrier), 2 cta engine, 3 dense GEMM
+  bool dense_large = false;
+  // dense GEMM engine buffers
+  double *d_Ar = nullptr, *d_Ai = nullptr;
+  std::vector<double*> d_Acr, d_Aci;
+  double2 *dd_st = nullptr, *dd_nx = nullptr, *dd_cur = nullptr, *dd_tb0 = nullptr, *dd_tb1 = nullptr,
+          *dd_xcur = nullptr, *dd_xtb0 = nullptr, *dd_xtb1 = nullptr, *dd_tmp = nullptr;
+  double2* dd_dots = nullptr;
+  double dense_dt = NAN;
+  std::vector<double2*> d_hc_dense_host;
+  int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
+  int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
+  bool ws_cluster = false;
+  double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
+  size_t splitws_cap = 0;
+  // cluster engine
+  int cl_CS = 0, cl_R = 0, cl_H = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
+  int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
+  unsigned char* d_cl_slot = nullptr;
+  int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
+  long scratch_per_group = 0;
+  std::vector<int> grp_set, grp_t0, grp_nT;
+  int live_peak = 0;
+  long shard_b = 0, shard_e = 1L << 40;
+  // device: static
+  DevMem mem;
+  cudaStream_t stream = nullptr;
+  int *d_rowlen = nullptr, *d_cols = nullptr, *d_src_s = nullptr, *d_src_c = nullptr, *d_colptr = nullptr,
+      *d_colent = nullptr;
+  double2* d_hs = nullptr;
+  double2** d_hc_ptrs = nullptr;
+  double2* d_hs_dense = nullptr;
+  double2** d_hc_dense_ptrs = nullptr;
+  int* d_ccols = nullptr;
+  double2* d_traj = nullptr;
+  double2* d_scratch = nullptr;
+  unsigned* d_bar = nullptr;
+  double2* d_red = nullptr;
+  // per-dt control data
+  double cached_dt = NAN;
+  DevMem dtmem;
+  double2* d_Ac = nullptr;
+  double *d_ctrl_col = nullptr, *d_ctrl_row = nullptr, *d_ac_abs = nullptr, *d_ac_abs_dense = nullptr;
+  int *d_ctrl_nnz = nullptr, *d_ac_rowlen = nullptr;
+  // per-N buffers
+  long capN = 0;
+  DevMem nmem;
+  double* d_amps = nullptr;
+  double2* d_A = nullptr;
+  double *d_norm1 = nullptr, *d_aux_arg = nullptr, *d_parg = nullptr;
+  long long *d_sp = nullptr, *d_aux_sp = nullptr, *d_psp = nullptr;
+  int4* d_plan = nullptr;
+  int* d_flag = nullptr;
+  double2 *d_ip = nullptr, *d_fin = nullptr, *d_trp = nullptr, *d_trsum = nullptr, *d_psiN = nullptr;
+  // sharded evaluation: raw scalars [ip | fin | trp | run] in one (optionally caller-lent) buffer and
+  // the caller's all-reduce hook (lg_eval_sharded)
+  double* d_raw = nullptr;
+  double* ext_raw = nullptr;
+  long ext_raw_len = 0;
+  lg_allreduce_fn hook = nullptr;
+  void* hook_user = nullptr;
+  bool trp_reduced = false;
+  bool has_gate_run = false;
+  double *d_run = nullptr, *d_grad = nullptr, *d_cost = nullptr;
+  int *d_spec_t0 = nullptr, *d_spec_K = nullptr;
+  long lastN = 0;
+  bool own_stream = true;
+  bool timing = false;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double phase_ms[4] = {0, 0, 0, 0};
+  long timed_evals = 0;
+
+  ~lg_problem() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    nmem.release();
+    dtmem.release();
+    mem.release();
+    if (d_splitws) cudaFree(d_splitws);
+    if (stream && own_stream) cudaStreamDestroy(stream);
+  }
+  void mark(int i) {
+    if (timing) cudaEventRecord(ev[i], stream);
+  }
+  void collect() {
+    if (!timing) return;
+    cudaEventSynchronize(ev[4]);
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      phase_ms[i] += ms;
+    }
+    ++timed_evals;
+  }
+};
+
+namespace lgi {
+
+extern long long g_launches;  // kernels launched by this library (lg_launch_count)
+
+// lg_host.cu: problem ingestion and per-evaluation preparation
+int build_problem(const lg_problem_desc* D, lg_problem* p);
+int prepare_dt(lg_problem* p, double dt);
+int ensure_N(lg_problem* p, long N);
+int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop = false);
+int prepare_steps(lg_problem* p, long N, double dt, bool need_aux);
+LgEngineArgs engine_args(lg_problem* p, long N);
+LgFinalArgs final_args(lg_problem* p, long N, const double2* ip, const double2* fin, const double* run,
+                       const double2* trp, double* grad, double* cost);
+
+// lg_configure.cu: engine selection
+int configure(lg_problem* p);
+std::vector<int> rcm_order(long d, const std::vector<std::vector<int>>& adj);
+void cl_color_slots(long d, int W, int R, const std::vector<int>& perm, const std::vector<int>& rowlen,
+                    const std::vector<int>& cp, std::vector<int>& ncol, std::vector<unsigned char>& nslot);
+
+// lg_dense_host.cu: dense (DMMA) engine driver
+int configure_dense(lg_problem* p);
+int run_dense(lg_problem* p, long N, double dt, bool grad);
+int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2* X, const double* Br,
+               const double* Bi, const double2* Xb, int C, double r, bool first, bool last, const double2* xin,
+               double2* cur, double2* tout);
+
+}  // namespace lgi

@@ -116,3 +116,59 @@ struct LgFinalArgs {
   double* grad;   // [N][Kc]
   double* cost;   // [1]
 };
+
+// ---- host <-> dense-path kernel arguments (lg_dense.cu; filled by the host units)
+struct LgGemmSeg {
+  const double* Ar;
+  const double* Ai;
+  int lda;
+  const double2* X;
+  int ldx;
+  int K;
+};
+struct LgGemmArgs {
+  int M, C;
+  LgGemmSeg seg[2];
+  int nseg;
+  const double2* xin;
+  int ldxin;
+  double2* cur;
+  int ldc;
+  double2* tout;
+  int ldt;
+  double r;
+  int first, last;
+  int ksplit;  // lg_dense.cu: split-k slices (partial products in `partial`)
+  double2* partial;
+};
+struct LgDotArgs {
+  int d, n;
+  const double2* u[64];
+  const double2* v[64];
+  double2* out[64];
+};
+struct LgEllArgs {
+  int d, W, ncol, accumulate;
+  const int* cols;
+  const double2* vals;
+  const double2* x[64];
+  double2* y[64];
+};
+struct LgAxpyArgs {
+  int d, ncol;
+  const double2* u[64];
+  double2* y[64];
+  double2 alpha[64];
+  const double2* alpha_ptr[64];
+  int accumulate[64];
+};
+struct LgEllTaylorArgs {  // lg_dense.cu
+  int d, W, ncol, first, last;
+  double r;
+  const int* cols;
+  const double2* vals;
+  const double2* X;
+  const double2* xin;
+  double2* cur;
+  double2* T;
+};
