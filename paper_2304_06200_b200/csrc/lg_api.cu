@@ -143,13 +143,14 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       if (rc) return rc;
     } else if (p->engine == 4 && p->ws_cluster) {
       cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(p->n_groups * (p->Kc + 1));
+      const int csz = 1 + p->cta_Imax + p->Kc * p->ws_nw;
+      cfg.gridDim = dim3(p->n_groups * csz);
       cfg.blockDim = bblock;
       cfg.dynamicSmemBytes = bsm;
       cfg.stream = p->stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = p->Kc + 1;
+      at[0].val.clusterDim.x = csz;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;

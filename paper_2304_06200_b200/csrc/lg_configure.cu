@@ -275,6 +275,8 @@ bool configure_cl(lg_problem* p, int smem_optin) {
 }
 
 // Warp-specialised engine (lg_sweep_ws.cu): small sparse problems, one CTA per trajectory.
+constexpr int RING_WS = 4;  // lg_sweep_ws.cu RING
+
 bool configure_ws(lg_problem* p, int smem_optin) {
   if (p->dense || p->W > 9 || p->d > 64 || p->Wc > 2 || p->Kc > 6) return false;
   int nspec[2] = {0, 0};
@@ -296,15 +298,23 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   }
   if (gset.empty() || gset.size() > 64) return false;
   const int rpl = p->d <= 64 ? 1 : 2;
-  const int fw = lg_ws_layout_words((int)p->d, 2, Imax, Wp), bw = lg_ws_layout_words((int)p->d, p->Kc + 1 + Imax, Imax, Wp);
+  const int fw = lg_ws_layout_words((int)p->d, 2, Imax, Wp, 0), bw = lg_ws_layout_words((int)p->d, p->Kc + 1 + Imax, Imax, Wp, 0);
   if ((long)std::max(fw, bw) * 16 > std::min(smem_optin, 227 * 1024)) return false;
   void* f0 = lg_ws_kernel(0, p->W, rpl);
   void* f1 = lg_ws_kernel(1, p->W, rpl);
   if (!f0 || !f1) return false;
   // cluster variant: one CTA per derivative team + one for psi/costates
   const char* nc = std::getenv("LG_WS_NOCLUSTER");
-  const int cw = lg_ws_layout_words((int)p->d, 1 + Imax, Imax, Wp);
-  p->ws_cluster = !nc && p->Kc + 1 <= 8 && (long)cw * 16 <= std::min(smem_optin, 227 * 1024);
+  // NW derivative workers per channel take the per-step aux chains off the sequential psi / costate
+  // critical path (a portable cluster holds 1 + Kc * NW <= 8 CTAs)
+  // cluster = psi rank + one rank per costate + NW derivative workers per channel (<= 16 CTAs,
+  // non-portable size)
+  int nw = std::max(1, std::min(3, (15 - Imax) / std::max(p->Kc, 1)));
+  if (const char* e = std::getenv("LG_WS_NW")) nw = std::max(1, std::atoi(e));
+  while (nw > 1 && 1 + Imax + p->Kc * nw > 16) --nw;
+  const int cw = lg_ws_layout_words((int)p->d, 1, Imax, Wp, 2 * RING_WS + p->Kc * nw * 4 * (1 + Imax));
+  p->ws_nw = nw;
+  p->ws_cluster = !nc && 1 + Imax + p->Kc * nw <= 16 && (long)cw * 16 <= std::min(smem_optin, 227 * 1024);
   if (p->ws_cluster) {
     void* f2 = lg_ws_kernel(2, p->W, rpl);
     if (!f2 || cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, cw * 16) != cudaSuccess)
@@ -320,7 +330,8 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   p->ws_rpl = rpl;
   p->ws_fwd_smem = fw * 16;
   p->ws_bwd_smem = bw * 16;
-  p->ws_bwd_threads = p->ws_cluster ? std::max(160, (1 + Imax) * 64) : (p->Kc + 1 + Imax) * 64;
+  p->ws_bwd_threads = p->ws_cluster ? 160 : (p->Kc + 1 + Imax) * 64;
+  p->cta_Imax = Imax;
   if (p->ws_cluster) p->ws_bwd_smem = cw * 16;
   p->threads = 128;
   p->n_slabs = 1;

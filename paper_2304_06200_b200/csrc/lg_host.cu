@@ -342,6 +342,7 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.cl_R = p->cl_R;
   E.cl_H = p->cl_H;
   E.cl_acs = 0;
+  E.ws_nw = p->ws_nw;
   E.dense_rows = (p->dense && p->W == p->d && p->Wc == p->d) ? 1 : 0;
   E.cl_perm = p->d_cl_perm;
   E.cl_inv = p->d_cl_inv;

@@ -35,7 +35,7 @@ extern "C" void* lg_taylor_epi_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc);
 extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
-extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp);
+extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars);
 extern "C" void* lg_dense_form_kernel();
 extern "C" void* lg_dots_kernel();
 extern "C" void* lg_ell_kernel();
@@ -141,6 +141,7 @@ struct lg_problem {
   int cta_maxr = 1, cta_maxc = 1, cta_wreg = 0, row_lanes = 32, cta_Imax = 1;
   int ws_rpl = 1, ws_fwd_smem = 0, ws_bwd_smem = 0, ws_bwd_threads = 0;
   bool ws_cluster = false;
+  int ws_nw = 1;  // derivative workers per channel in the cluster backward
   double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
   size_t splitws_cap = 0;
   // cluster engine

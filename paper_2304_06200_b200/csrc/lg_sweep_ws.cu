@@ -264,7 +264,7 @@ struct WsLay {
   int words;
 };
 
-__host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, int Wp) {
+__host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, int Wp, int extra_bars = 0) {
   WsLay L;
   int o = 0;
   L.tb = o;
@@ -283,10 +283,10 @@ __host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, in
   o += I * Wp * d;
   L.pencol = o;
   o += (I * Wp * d + 3) / 4;
-  L.dbuf = o;  // [2][d] derivative columns handed from the X team to its dot warp (cluster kernel)
-  o += 2 * d;
+  L.dbuf = o;  // [4][d] derivative columns handed from the X team to its dot warp (cluster kernel)
+  o += 4 * d;
   L.bars = o;
-  o += (2 * RING * (1 + I) + 4 + 1) / 2 + 1;
+  o += (2 * RING * (1 + I) + 4 + extra_bars + 1) / 2 + 1;
   L.words = o;
   return L;
 }
@@ -675,28 +675,42 @@ __global__ void __launch_bounds__(512, 1) lg_k_ws_backward(const __grid_constant
 }
 
 // ------------------------------------------------------------------------------------------ backward (cluster)
-// Cluster of 1 + Kc CTAs per trajectory.  Rank 0: psi team P and costate teams
-// L_s (two warps each); rank 1 + k: derivative team X_k alone on its SM.  P and
-// L_s push psi_{n-1} / lambda_s(n) rows into every X CTA's ring over DSMEM and
-// arrive remotely on that CTA's full barrier; X CTAs arrive remotely on rank 0's
-// empty barriers.  All waits acquire at cluster scope.
+// Cluster of 1 + Imax + Kc * NW CTAs per trajectory, every chain on its own SM.  Rank 0: psi-recovery
+// team P (inverse propagation, src/costs.py:326).  Rank 1 + s: costate team L_s (src/costs.py:341-353).
+// Rank 1 + Imax + k * NW + w: derivative worker
+// of channel k for the backward steps it = w (mod NW): the aux chain of step n needs only psi_{n-1}
+// and A_n (src/costs.py:328-331), so NW workers take a channel's derivative chains off the
+// sequential psi / lambda critical path.  Each worker: X team (four warps: top | bottom column of
+// the block operator) + a dot-product warp for <lambda_s(n)|dU_n/da_k psi_{n-1}>.  P and L_s
+// st.async psi_{n-1} / lambda_s(n) rows into the responsible worker's 2-slot ring
+// (mbarrier complete_tx); workers free slots with relaxed remote arrives.
+constexpr int WR = 4;  // ring slots per worker (psi / lambda) and derivative hand-off depth
 template <int W>
 __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constant__ LgEngineArgs E) {
-  const int d = E.d, Kc = E.Kc, N = E.N;
+  const int d = E.d, Kc = E.Kc, N = E.N, NW = E.ws_nw, NWK = Kc * E.ws_nw, IM = E.cta_Imax;
   const unsigned rank = cl_rank();
-  const int g = blockIdx.x / (Kc + 1);
+  const int g = blockIdx.x / (1 + IM + NWK);
+  const int xr0 = 1 + IM;  // first worker rank
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set];
   int Wp = 1;
   for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
-  const WsLay L = ws_layout(d, 1 + I, I, Wp);
+  const WsLay L = ws_layout(d, 1, IM, Wp, 2 * RING + NWK * WR * (1 + IM));
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
-  unsigned long long* pfull = bars;               // [RING]  (every rank)
-  unsigned long long* pempty = bars + RING;       // [RING]  (rank 0)
-  unsigned long long* lfull = bars + 2 * RING;    // [I][RING] (X ranks)
-  unsigned long long* lempty = lfull + I * RING;  // [I][RING] (rank 0)
-  unsigned long long* dfull = lempty + I * RING;  // [2] X team -> dot warp (X ranks)
-  unsigned long long* dempty = dfull + 2;         // [2] dot warp -> X team
+  // rank 0 (P): costate ranks free psi slots; workers free their psi slots
+  unsigned long long* pempty = bars;                  // [RING]
+  unsigned long long* wempty = bars + RING;           // [NWK][WR]
+  // costate rank 1 + s: psi_{n-1} arrived (penalty / running sources); workers free lambda slots;
+  // source ring between the source warp and the costate team
+  unsigned long long* pfull = bars;                   // [RING]
+  unsigned long long* lempty = bars + RING;           // [NWK][WR]
+  unsigned long long* sfull = lempty + NWK * WR;      // [RING]
+  unsigned long long* sempty = sfull + RING;          // [RING]
+  // workers
+  unsigned long long* xfull = bars;                   // [WR] psi_{n-1} arrived
+  unsigned long long* lfull = bars + WR;              // [I][WR] lambda_s(n) arrived
+  unsigned long long* dfull = lfull + I * WR;         // [WR] X team -> dot warp
+  unsigned long long* dempty = dfull + WR;            // [WR] dot warp -> X team
   int* pcol = reinterpret_cast<int*>(ws_sm) + 4 * L.pencol;
   const int team = threadIdx.x >> 6, tl = threadIdx.x & 63;
   const Team tm{team + 1, tl, 64, d};
@@ -707,30 +721,32 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   }
   stage_specs(E, L, set, trel, I, Wp, pcol);
   if (threadIdx.x == 0) {
-    // rank 0: pfull counts the 64 local P arrivals; X ranks: full barriers are armed by one
-    // expect_tx arrival per phase and completed by the producers' st.async bytes
-    for (int j = 0; j < RING; ++j) {
-      mb_init(&pfull[j], rank == 0 ? 64 : 1);
-      mb_init(&pempty[j], Kc + n_lpsi);
-      for (int si = 0; si < I; ++si) {
-        mb_init(&lfull[si * RING + j], rank == 0 ? 64 : 1);
-        mb_init(&lempty[si * RING + j], Kc);
+    if (rank == 0) {
+      for (int j = 0; j < RING; ++j) mb_init(&pempty[j], n_lpsi > 0 ? n_lpsi : 1);
+      for (int q = 0; q < NWK * WR; ++q) mb_init(&wempty[q], 1);
+    } else if (rank < (unsigned)xr0) {
+      for (int j = 0; j < RING; ++j) {
+        mb_init(&pfull[j], 1);  // armed by expect_tx
+        mb_init(&sfull[j], 32);
+        mb_init(&sempty[j], 1);
       }
-    }
-    for (int b = 0; b < 2; ++b) {
-      mb_init(&dfull[b], 1);
-      mb_init(&dempty[b], 1);
+      for (int q = 0; q < NWK * WR; ++q) mb_init(&lempty[q], 1);
+    } else {
+      for (int j = 0; j < WR * (1 + I); ++j) mb_init(&xfull[j], 1);  // xfull and lfull: armed by expect_tx
+      for (int b = 0; b < WR; ++b) {
+        mb_init(&dfull[b], 1);
+        mb_init(&dempty[b], 1);
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   cl_sync();
   const int i = tl;
-  const int tb0 = L.tb + team * 4 * d, tb1 = tb0 + 2 * d, rt = L.rt + team * 64;
-  const int red = L.red + team * 2 * LG_MAX_SPECS;
-  if (rank > 0 && threadIdx.x < 128) {
-    // ---------------- X_k on its own SM: four warps (top column | bottom column)
-    const int kch = rank - 1;
+  const int tb0 = L.tb, tb1 = tb0 + 2 * d, rt = L.rt, red = L.red;  // one team per CTA
+  if (rank >= (unsigned)xr0 && threadIdx.x < 128) {
+    // ---------------- X: derivative worker (channel kch, steps it = w mod NW), four warps
+    const int wi = rank - xr0, kch = wi / NW, w0 = wi % NW;
     const int t4 = threadIdx.x;
     const bool top = t4 < 64;
     const int ix = t4 & 63;
@@ -752,23 +768,19 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
         cc[w] = ix < d ? E.A_cols[w * d + ix] : 0;
       }
     };
-    rows(N - 1, an, coln);
-    int4 pln = E.plan[(long)(N - 1) * (Kc + 1) + 1 + kch];
+    if (w0 < N) rows(N - 1 - w0, an, coln);
     const int xb0 = L.tb, xb1 = L.tb + 2 * d, xrt = L.rt;
-    for (int it = 0; it < N; ++it) {
+    for (int it = w0, u = 0; it < N; it += NW, ++u) {
       const int n = N - 1 - it;
-      const int4 pl = pln;
+      const int4 pl = E.plan[(long)n * (Kc + 1) + 1 + kch];
 #pragma unroll
       for (int w = 0; w < W; ++w) a[w] = an[w], col[w] = coln[w];
-      if (n > 0) {
-        rows(n - 1, an, coln);
-        pln = E.plan[(long)(n - 1) * (Kc + 1) + 1 + kch];
-      }
-      const int slot = it % RING, use = it / RING;
-      long long* trc = E.trace ? E.trace + (((long)g * 8 + kch) * N + it) * 4 : nullptr;
+      if (it + NW < N) rows(n - NW, an, coln);
+      const int slot = u % WR;
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + wi) * N + it) * 4 : nullptr;
       if (trc && t4 == 0) trc[0] = clock64();
-      if (t4 == 0) mb_expect_tx(&pfull[slot], (unsigned)d * 16u);
-      mb_wait(&pfull[slot], use & 1);
+      if (t4 == 0) mb_expect_tx(&xfull[slot], (unsigned)d * 16u);
+      mb_wait(&xfull[slot], (u / WR) & 1);
       if (trc && t4 == 0) trc[1] = clock64();
       double2 cur = make_double2(0.0, 0.0);
       if (ix < d) {
@@ -777,52 +789,58 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
         ws_sm[xb0 + (top ? 0 : d) + ix] = top ? make_double2(0.0, 0.0) : v0;
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (t4 == 0) cl_arrive_relaxed(cl_map(&pempty[slot], 0));
+      if (t4 == 0) cl_arrive_relaxed(cl_map(&wempty[wi * WR + slot], 0));
       x4_chain<W>(1, ix, d, top, cur, a, col, ac, accol, pl.x, pl.y, xb0, xb1, xrt, t4);
       if (trc && t4 == 0) trc[2] = clock64();
-      // hand D_k (top column) to the dot warp; it reduces <lambda_s(n)|D_k> off this critical path
-      const int b = it & 1;
-      if (it >= 2) mb_wait(&dempty[b], ((it >> 1) - 1) & 1);
+      // hand D_k to the dot warp
+      const int b = u % WR;
+      if (u >= WR) mb_wait(&dempty[b], ((u / WR) - 1) & 1);
       if (top && ix < d) ws_sm[L.dbuf + b * d + ix] = cur;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
       if (t4 == 0) mb_arrive(&dfull[b]);
       if (trc && t4 == 0) trc[3] = clock64();
     }
-  } else if (rank > 0 && threadIdx.x < 160) {
-    // ---------------- dot warp of X_k: ip[n][s][k] = <lambda_s(n) | dU_n/da_k psi_{n-1}>
-    const int kch = rank - 1;
+  } else if (rank >= (unsigned)xr0 && threadIdx.x < 160) {
+    // ---------------- dot warp of the worker: ip[n][s][k] = <lambda_s(n) | dU_n/da_k psi_{n-1}>
+    const int wi = rank - xr0, kch = wi / NW, w0 = wi % NW;
     const int lane = threadIdx.x - 128;
-    for (int it = 0; it < N; ++it) {
+    for (int it = w0, u = 0; it < N; it += NW, ++u) {
       const int n = N - 1 - it;
-      const int slot = it % RING, use = it / RING, b = it & 1;
-      if (lane < I) mb_expect_tx(&lfull[lane * RING + slot], (unsigned)d * 16u);
-      mb_wait(&dfull[b], (it >> 1) & 1);
+      const int slot = u % WR, b = u % WR;
+      if (lane < I) mb_expect_tx(&lfull[lane * WR + slot], (unsigned)d * 16u);
+      mb_wait(&dfull[b], (u / WR) & 1);
       double2 v[LG_MAX_SPECS];
       for (int si = 0; si < I; ++si) {
-        mb_wait(&lfull[si * RING + slot], use & 1);
+        mb_wait(&lfull[si * WR + slot], (u / WR) & 1);
         double2 acc = make_double2(0.0, 0.0);
         for (int i2 = lane; i2 < d; i2 += 32)
-          acc = cadd(acc, cdot(ws_sm[L.lring + (si * RING + slot) * d + i2], ws_sm[L.dbuf + b * d + i2]));
+          acc = cadd(acc, cdot(ws_sm[L.lring + (si * WR + slot) * d + i2], ws_sm[L.dbuf + b * d + i2]));
         v[si] = warp_sum(acc);
       }
       __syncwarp();
       if (lane == 0) {
         mb_arrive(&dempty[b]);
         for (int si = 0; si < I; ++si) {
-          cl_arrive_relaxed(cl_map(&lempty[si * RING + slot], 0));
+          cl_arrive_relaxed(cl_map(&lempty[wi * WR + slot], 1 + si));
           const int sidx = E.set_spec[set][si];
           E.ip[(((long)n * E.n_specs + sidx) * Kc + kch) * E.T_total + t0] = v[si];
         }
       }
       __syncwarp();
     }
-  } else if (rank == 0 && team == 0) {
-    // ---------------- P: psi recovery; pushes psi_{n-1} to every X CTA
+  } else if (rank == 0 && threadIdx.x < 64) {
+    // ---------------- P: psi recovery; pushes psi_{n-1} to the costate ranks that need it and to the
+    // step's workers (one per channel)
     double2 cur[1][1];
     double2 a[1][W], an[1][W];
     int col[1][W], coln[1][W];
     const double2 ac[1][2] = {};
     const int accol[1][2] = {};
+    unsigned lpsi = 0;  // costate ranks with psi-dependent sources
+    for (int si = 0; si < I; ++si) {
+      const int kind = E.spec[E.set_spec[set][si]].kind;
+      if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN) lpsi |= 1u << si;
+    }
     if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
     load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
@@ -837,25 +855,31 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
         pln = E.plan[(long)(n - 1) * (Kc + 1)];
       }
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
-      long long* trc = E.trace ? E.trace + (((long)g * 8 + Kc) * N + it) * 4 : nullptr;
+      long long* trc = E.trace ? E.trace + (((long)g * 8 + 7) * N + it) * 4 : nullptr;
       if (trc && tl == 0) trc[0] = clock64();
       team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[1] = clock64();
+      const int w0 = it % NW, u = it / NW, wslot = u % WR;
+      for (int k = 0; k < Kc; ++k)  // the workers' slots are free (they took psi of step it - WR * NW)
+        if (u >= WR) mb_wait(&wempty[(k * NW + w0) * WR + wslot], ((u / WR) - 1) & 1);
       const int slot = it % RING, use = it / RING;
-      if (use > 0) mb_wait(&pempty[slot], (use - 1) & 1);
+      if (lpsi && use > 0) mb_wait(&pempty[slot], (use - 1) & 1);
       if (trc && tl == 0) trc[2] = clock64();
       if (i < d) {
-        ws_sm[L.ring + slot * d + i] = cur[0][0];
         ws_sm[tb0 + i] = cur[0][0];
-        for (int r = 1; r <= Kc; ++r)
-          cl_st_async(cl_map(&ws_sm[L.ring + slot * d + i], r), cur[0][0], cl_map(&pfull[slot], r));
+        for (int k = 0; k < Kc; ++k) {
+          const int r = xr0 + k * NW + w0;
+          cl_st_async(cl_map(&ws_sm[L.ring + wslot * d + i], r), cur[0][0], cl_map(&xfull[wslot], r));
+        }
+        for (int si = 0; si < I; ++si)
+          if (lpsi & (1u << si))
+            cl_st_async(cl_map(&ws_sm[L.ring + slot * d + i], 1 + si), cur[0][0], cl_map(&pfull[slot], 1 + si));
       }
-      mb_arrive(&pfull[slot]);
       team_sync(tm.id);
     }
-  } else if (rank == 0 && team <= I) {
-    // ---------------- L_s: costate chain + sources; pushes lambda_s(n) to every X CTA
-    const int si = team - 1;
+  } else if (rank >= 1 && rank < (unsigned)(1 + I) && threadIdx.x < 64) {
+    // ---------------- L_s on its own SM: costate chain + sources; pushes lambda_s(n) to the step's workers
+    const int si = rank - 1;
     const int sidx = E.set_spec[set][si];
     const int kind = E.spec[sidx].kind;
     const bool needs_psi = kind == LGK_STATE_PEN || kind == LGK_STATE_RUN;
@@ -895,12 +919,19 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int slot = it % RING, use = it / RING;
-      if (use > 0) mb_wait(&lempty[si * RING + slot], (use - 1) & 1);
+      const int w0 = it % NW, u = it / NW, wslot = u % WR;
+      long long* trc = (E.trace && si < 2) ? E.trace + (((long)g * 8 + 6 - si) * N + it) * 4 : nullptr;
+      if (trc && tl == 0) trc[0] = clock64();
+      for (int k = 0; k < Kc; ++k)
+        if (u >= WR) mb_wait(&lempty[(k * NW + w0) * WR + wslot], ((u / WR) - 1) & 1);
+      if (trc && tl == 0) trc[1] = clock64();
       if (i < d) {
         ws_sm[tb0 + i] = cur[0][0];
-        for (int r = 1; r <= Kc; ++r)
-          cl_st_async(cl_map(&ws_sm[L.lring + (si * RING + slot) * d + i], r), cur[0][0],
-                      cl_map(&lfull[si * RING + slot], r));
+        for (int k = 0; k < Kc; ++k) {
+          const int r = xr0 + k * NW + w0;
+          cl_st_async(cl_map(&ws_sm[L.lring + (si * WR + wslot) * d + i], r), cur[0][0],
+                      cl_map(&lfull[si * WR + wslot], r));
+        }
       }
       if (n == 0) break;
       const int4 pl = pln;
@@ -911,21 +942,45 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
       team_sync(tm.id);
       team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
-      if (needs_psi) {
+      if (trc && tl == 0) trc[2] = clock64();
+      if (needs_psi) {  // source at psi_{n-1} (src/costs.py:341-353), formed by the source warp
+        mb_wait(&sfull[slot], use & 1);
+        if (i < d) cur[0][0] = cadd(cur[0][0], ws_sm[L.lring + slot * d + i]);
+        team_sync(tm.id);
+        if (tl == 0) mb_arrive(&sempty[slot]);
+        if (trc && tl == 0) trc[3] = clock64();
+      } else if (kind == LGK_GATE_RUN) {
+        if (i < d) cur[0][0] = cadd(cur[0][0], cmul(ws_sm[tg + i], tr));
+      }
+    }
+  } else if (rank >= 1 && rank < (unsigned)(1 + I) && threadIdx.x >= 64 && threadIdx.x < 96) {
+    // ---------------- source warp of L_s: Omega psi_{n-1} or phi <phi|psi_{n-1}> as soon as P delivers
+    // psi_{n-1}; the costate team adds it after its chain (same operation order as src/costs.py:341-353)
+    const int si = rank - 1;
+    const int sidx = E.set_spec[set][si];
+    const int kind = E.spec[sidx].kind;
+    if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN) {
+      const int tg = L.tgt + si * d;
+      const int pen = L.pen + si * Wp * d;
+      const int* pc = pcol + si * Wp * d;
+      const int lane = threadIdx.x - 64;
+      for (int it = 0; it + 1 < N; ++it) {  // lambda(n-1) needs the source for n = N-1 .. 1
+        const int slot = it % RING, use = it / RING;
+        if (use > 0) mb_wait(&sempty[slot], (use - 1) & 1);
+        if (lane == 0) mb_expect_tx(&pfull[slot], (unsigned)d * 16u);
         mb_wait(&pfull[slot], use & 1);
         const int psi = L.ring + slot * d;
         if (kind == LGK_STATE_RUN) {
-          double2 o2[1] = {make_double2(0.0, 0.0)};
-          if (i < d) o2[0] = cdot(ws_sm[tg + i], ws_sm[psi + i]);
-          team_reduce<1>(tm, o2, 1, red);
-          if (i < d) cur[0][0] = cadd(cur[0][0], cmul(ws_sm[tg + i], o2[0]));
+          double2 o = make_double2(0.0, 0.0);
+          for (int r = lane; r < d; r += 32) o = cadd(o, cdot(ws_sm[tg + r], ws_sm[psi + r]));
+          o = warp_sum(o);
+          for (int r = lane; r < d; r += 32) ws_sm[L.lring + slot * d + r] = cmul(ws_sm[tg + r], o);
         } else {
-          if (i < d) cur[0][0] = cadd(cur[0][0], pen_row(d, Wp, pen, pc, i, psi));
+          for (int r = lane; r < d; r += 32) ws_sm[L.lring + slot * d + r] = pen_row(d, Wp, pen, pc, r, psi);
         }
-        team_sync(tm.id);
-        if (tl == 0) mb_arrive(&pempty[slot]);
-      } else if (kind == LGK_GATE_RUN) {
-        if (i < d) cur[0][0] = cadd(cur[0][0], cmul(ws_sm[tg + i], tr));
+        __syncwarp();
+        if (lane == 0) cl_arrive_relaxed(cl_map(&pempty[slot], 0));
+        mb_arrive(&sfull[slot]);
       }
     }
   }
@@ -933,7 +988,9 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   cl_sync();  // no CTA leaves while its shared memory may still be addressed remotely
 }
 
-extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp) { return ws_layout(d, nteams, I, Wp).words; }
+extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars) {
+  return ws_layout(d, nteams, I, Wp, extra_bars).words;
+}
 
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl) {
   (void)rpl;

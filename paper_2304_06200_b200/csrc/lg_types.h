@@ -96,6 +96,7 @@ struct LgEngineArgs {
   // cluster engine (lg_sweep_cl.cu): RCM renumbering of the rows
   int cl_R, cl_H;           // rows per CTA, halo width (bandwidth of the renumbered pattern)
   int cl_acs;               // backward stages the control-generator rows in shared memory
+  int ws_nw;                // ws cluster backward: derivative workers per control channel
   int dense_rows;           // every operator row stores all d columns in order (dense H): slot w == column w
   const int* cl_perm;       // [d] renumbered row -> original row
   const int* cl_inv;        // [d] original row -> renumbered row
