@@ -278,7 +278,11 @@ bool configure_cl(lg_problem* p, int smem_optin) {
 constexpr int RING_WS = 4;  // lg_sweep_ws.cu RING
 
 bool configure_ws(lg_problem* p, int smem_optin) {
-  if (p->dense || p->W > 9 || p->d > 64 || p->Wc > 2 || p->Kc > 6) return false;
+  // dense rows (d <= 64): the step operators are staged in shared memory, cluster backward only
+  const int dns = p->dense ? 1 : 0;
+  if (p->d > 64 || p->Kc > 6) return false;
+  if (dns ? (p->dense_large || p->W != p->d || p->Wc != p->d) : (p->W > 9 || p->Wc > 2)) return false;
+  const int kw = dns ? 0 : p->W;
   int nspec[2] = {0, 0};
   int Wp = 1;
   for (auto& s : p->specs) {
@@ -298,11 +302,12 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   }
   if (gset.empty() || gset.size() > 64) return false;
   const int rpl = p->d <= 64 ? 1 : 2;
-  const int fw = lg_ws_layout_words((int)p->d, 2, Imax, Wp, 0), bw = lg_ws_layout_words((int)p->d, p->Kc + 1 + Imax, Imax, Wp, 0);
+  const int fw = lg_ws_layout_words((int)p->d, 2, Imax, Wp, 0, dns);
+  const int bw = dns ? 0 : lg_ws_layout_words((int)p->d, p->Kc + 1 + Imax, Imax, Wp, 0, 0);
   if ((long)std::max(fw, bw) * 16 > std::min(smem_optin, 227 * 1024)) return false;
-  void* f0 = lg_ws_kernel(0, p->W, rpl);
-  void* f1 = lg_ws_kernel(1, p->W, rpl);
-  if (!f0 || !f1) return false;
+  void* f0 = lg_ws_kernel(0, kw, rpl);
+  void* f1 = lg_ws_kernel(1, kw, rpl);
+  if (!f0 || (!f1 && !dns)) return false;
   // cluster variant: one CTA per derivative team + one for psi/costates
   const char* nc = std::getenv("LG_WS_NOCLUSTER");
   // NW derivative workers per channel take the per-step aux chains off the sequential psi / costate
@@ -312,18 +317,19 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   int nw = std::max(1, std::min(3, (15 - Imax) / std::max(p->Kc, 1)));
   if (const char* e = std::getenv("LG_WS_NW")) nw = std::max(1, std::atoi(e));
   while (nw > 1 && 1 + Imax + p->Kc * nw > 16) --nw;
-  const int cw = lg_ws_layout_words((int)p->d, 1, Imax, Wp, 2 * RING_WS + p->Kc * nw * 4 * (1 + Imax));
+  const int cw = lg_ws_layout_words((int)p->d, 1, Imax, Wp, 2 * RING_WS + p->Kc * nw * 4 * (1 + Imax), dns);
   p->ws_nw = nw;
   p->ws_cluster = !nc && 1 + Imax + p->Kc * nw <= 16 && (long)cw * 16 <= std::min(smem_optin, 227 * 1024);
   if (p->ws_cluster) {
-    void* f2 = lg_ws_kernel(2, p->W, rpl);
+    void* f2 = lg_ws_kernel(2, kw, rpl);
     if (!f2 || cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, cw * 16) != cudaSuccess)
       p->ws_cluster = false;
     else
       cudaFuncSetAttribute(f2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
+  if (dns && !p->ws_cluster) return false;
   if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, fw * 16) != cudaSuccess ||
-      cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, bw * 16) != cudaSuccess)
+      (f1 && cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, bw * 16) != cudaSuccess))
     return false;
   p->engine = 4;
   p->multi = false;

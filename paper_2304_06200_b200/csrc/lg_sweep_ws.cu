@@ -164,6 +164,83 @@ __device__ __forceinline__ void team_chain(const Team& tm, double2 (&cur)[NC][RP
   }
 }
 
+// ---- dense rows (DenseMatrix problems, d <= 64): A_n is staged per step in shared memory,
+// column-major like the ELL table ([w][i], slot w == column w), one step ahead with cp.async.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+// Issue the copy of a d x d complex block (16-byte elements) into shared memory at `dst`.
+__device__ __forceinline__ void stage_block(const double2* src, int dst, int dd, int tid, int nthr) {
+  for (int q = tid; q < dd; q += nthr) cp_async16(&ws_sm[dst + q], src + q);
+  cp_async_commit();
+}
+// p = sum_w M[w][i] x[w] over a dense row, x read as a broadcast; four independent accumulators.
+__device__ __forceinline__ void dense_row(double2& p, double2& q, int mop, int xo, int i, int d) {
+  double2 p1 = make_double2(0.0, 0.0), q1 = p1, p2 = p1, q2 = p1, p3 = p1, q3 = p1;
+  int w = 0;
+  for (; w + 4 <= d; w += 4) {
+    cmac(p, q, ws_sm[mop + w * d + i], ws_sm[xo + w]);
+    cmac(p1, q1, ws_sm[mop + (w + 1) * d + i], ws_sm[xo + w + 1]);
+    cmac(p2, q2, ws_sm[mop + (w + 2) * d + i], ws_sm[xo + w + 2]);
+    cmac(p3, q3, ws_sm[mop + (w + 3) * d + i], ws_sm[xo + w + 3]);
+  }
+  for (; w < d; ++w) cmac(p, q, ws_sm[mop + w * d + i], ws_sm[xo + w]);
+  p = cadd(cadd(p, p1), cadd(p2, p3));
+  q = cadd(cadd(q, q1), cadd(q2, q3));
+}
+// Dense single-column team chain (propagation / adjoint / costate): operator at shared offset aop.
+__device__ __forceinline__ void team_chain_dense(const Team& tm, double2& cur, int aop, int m, int s, double sgn,
+                                                 int tb0, int tb1, int rt) {
+  if (tm.tl < m) ws_sm[rt + tm.tl].x = sgn * (1.0 / (double)(s * (tm.tl + 1)));
+  tsync(tm);
+  const int total = m * s, d = tm.d, i = tm.tl;
+  int X = tb0, Y = tb1, j = 1;
+  for (int t = 0; t < total; ++t) {
+    const double r = ws_sm[rt + j - 1].x;
+    const bool last = j == m;
+    if (i < d) {
+      double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
+      dense_row(p, q, aop, X, i, d);
+      const double2 tt = make_double2((p.x + q.x) * r, (p.y + q.y) * r);
+      cur = cadd(cur, tt);
+      ws_sm[Y + i] = last ? cur : tt;
+    }
+    tsync(tm);
+    const int t_ = X;
+    X = Y;
+    Y = t_;
+    j = last ? 1 : j + 1;
+  }
+}
+// Dense derivative chain on the four-warp team: top = A x_top + A_c x_bottom, bottom = A x_bottom.
+__device__ __forceinline__ void x4_chain_dense(int bar_id, int i, int d, bool top, double2& cur, int aop, int acop,
+                                               int m, int s, int tb0, int tb1, int rt, int tl) {
+  if (tl < m) ws_sm[rt + tl].x = 1.0 / (double)(s * (tl + 1));
+  asm volatile("bar.sync %0, 128;\n" ::"r"(bar_id) : "memory");
+  const int total = m * s;
+  const int c = top ? 0 : d;
+  int X = tb0, Y = tb1, j = 1;
+  for (int t = 0; t < total; ++t) {
+    const double r = ws_sm[rt + j - 1].x;
+    const bool last = j == m;
+    if (i < d) {
+      double2 p = make_double2(0.0, 0.0), q = make_double2(0.0, 0.0);
+      dense_row(p, q, aop, X + c, i, d);
+      if (top) dense_row(p, q, acop, X + d, i, d);
+      const double2 tt = make_double2((p.x + q.x) * r, (p.y + q.y) * r);
+      cur = cadd(cur, tt);
+      ws_sm[Y + c + i] = last ? cur : tt;
+    }
+    asm volatile("bar.sync %0, 128;\n" ::"r"(bar_id) : "memory");
+    const int t_ = X;
+    X = Y;
+    Y = t_;
+    j = last ? 1 : j + 1;
+  }
+}
+
 // Derivative team of four warps: warps 0-1 own the aux top column, warps 2-3
 // the bottom column, one row per lane.  Per term every thread first loads all
 // its operand slots, then accumulates, then stores (no store->load ordering
@@ -260,11 +337,13 @@ struct WsLay {
   int pen;     // penalty values: I x Wp x d ; cols as ints after
   int pencol;  // int offset (double2 units * 4 = int units)
   int dbuf;    // [2][d] derivative hand-off (cluster kernel)
+  int aop;     // dense rows: A_n double buffer [2][d][d] (column-major), then A_c of one channel [d][d]
   int bars;    // mbarriers
   int words;
 };
 
-__host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, int Wp, int extra_bars = 0) {
+__host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, int Wp, int extra_bars = 0,
+                                                    int dense = 0) {
   WsLay L;
   int o = 0;
   L.tb = o;
@@ -285,6 +364,8 @@ __host__ __device__ __forceinline__ WsLay ws_layout(int d, int nteams, int I, in
   o += (I * Wp * d + 3) / 4;
   L.dbuf = o;  // [4][d] derivative columns handed from the X team to its dot warp (cluster kernel)
   o += 4 * d;
+  L.aop = o;
+  if (dense) o += 3 * d * d;
   L.bars = o;
   o += (2 * RING * (1 + I) + 4 + extra_bars + 1) / 2 + 1;
   L.words = o;
@@ -320,14 +401,15 @@ __device__ __forceinline__ void stage_specs(const LgEngineArgs& E, const WsLay& 
 
 // ------------------------------------------------------------------------------------------ forward
 // warps 0-1: propagation team P; warps 2-3: per-step scalars team F.  d <= 64.
-template <int W>
+// DNS: dense rows (W unused), A_n staged in shared memory one step ahead.
+template <int W, int DNS>
 __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant__ LgEngineArgs E) {
-  const int d = E.d, g = blockIdx.x, N = E.N;
+  const int d = E.d, g = blockIdx.x, N = E.N, dd = d * d;
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set];
   int Wp = 1;
   for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
-  const WsLay L = ws_layout(d, 2, I, Wp);
+  const WsLay L = ws_layout(d, 2, I, Wp, 0, DNS);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
   unsigned long long* full = bars;
   unsigned long long* empty = bars + RING;
@@ -353,18 +435,28 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
     const double2 ac[1][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
     const int accol[1][2] = {{0, 0}};
     if (i < d) ws_sm[tb0 + i] = E.psi0[(long)t0 * d + i];
-    load_rows<W, 1>(E, 0, tm.tl, 64, an, coln);
+    if (DNS)
+      stage_block(E.A, L.aop, dd, tm.tl, 64);
+    else
+      load_rows<W, 1>(E, 0, tm.tl, 64, an, coln);
     int4 pln = E.plan[0];
     for (int n = 0; n < N; ++n) {
       const int4 pl = pln;
+      if (DNS) {
+        cp_async_wait_all();
+        tsync(tm);  // A_n staged; buffer (n + 1) & 1 no longer read (step n - 1 done)
+        if (n + 1 < N) stage_block(E.A + (long)(n + 1) * dd, L.aop + ((n + 1) & 1) * dd, dd, tm.tl, 64);
+      } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-      if (n + 1 < N) {
-        load_rows<W, 1>(E, n + 1, tm.tl, 64, an, coln);
-        pln = E.plan[(long)(n + 1) * (E.Kc + 1)];
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+        if (n + 1 < N) load_rows<W, 1>(E, n + 1, tm.tl, 64, an, coln);
       }
+      if (n + 1 < N) pln = E.plan[(long)(n + 1) * (E.Kc + 1)];
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
-      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+      if (DNS)
+        team_chain_dense(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+      else
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
       const int slot = n % RING, use = n / RING;
       if (use > 0) mb_wait(&empty[slot], (use - 1) & 1);
       if (i < d) {
@@ -685,9 +777,9 @@ __global__ void __launch_bounds__(512, 1) lg_k_ws_backward(const __grid_constant
 // st.async psi_{n-1} / lambda_s(n) rows into the responsible worker's 2-slot ring
 // (mbarrier complete_tx); workers free slots with relaxed remote arrives.
 constexpr int WR = 4;  // ring slots per worker (psi / lambda) and derivative hand-off depth
-template <int W>
+template <int W, int DNS>
 __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constant__ LgEngineArgs E) {
-  const int d = E.d, Kc = E.Kc, N = E.N, NW = E.ws_nw, NWK = Kc * E.ws_nw, IM = E.cta_Imax;
+  const int d = E.d, Kc = E.Kc, N = E.N, NW = E.ws_nw, NWK = Kc * E.ws_nw, IM = E.cta_Imax, dd = d * d;
   const unsigned rank = cl_rank();
   const int g = blockIdx.x / (1 + IM + NWK);
   const int xr0 = 1 + IM;  // first worker rank
@@ -695,7 +787,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   const int I = E.set_nspec[set];
   int Wp = 1;
   for (int si = 0; si < I; ++si) Wp = max(Wp, E.spec[E.set_spec[set][si]].pen_W);
-  const WsLay L = ws_layout(d, 1, IM, Wp, 2 * RING + NWK * WR * (1 + IM));
+  const WsLay L = ws_layout(d, 1, IM, Wp, 2 * RING + NWK * WR * (1 + IM), DNS);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ws_sm + L.bars);
   // rank 0 (P): costate ranks free psi slots; workers free their psi slots
   unsigned long long* pempty = bars;                  // [RING]
@@ -756,10 +848,11 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
     int accol[2];
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
-      const bool ok = top && ix < d && w < E.Wc;
+      const bool ok = !DNS && top && ix < d && w < E.Wc;
       ac[w] = ok ? E.Ac[((long)kch * E.Wc + w) * d + ix] : make_double2(0.0, 0.0);
       accol[w] = ok ? E.Ac_cols[((long)kch * E.Wc + w) * d + ix] : 0;
     }
+    if (DNS) stage_block(E.Ac + (long)kch * dd, L.aop + 2 * dd, dd, t4, 128);  // A_c of this channel
     auto rows = [&](int n, double2 (&aa)[W], int (&cc)[W]) {
       const double2* src = E.A + (long)n * W * d;
 #pragma unroll
@@ -768,14 +861,25 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
         cc[w] = ix < d ? E.A_cols[w * d + ix] : 0;
       }
     };
-    if (w0 < N) rows(N - 1 - w0, an, coln);
+    if (w0 < N) {
+      if (DNS)
+        stage_block(E.A + (long)(N - 1 - w0) * dd, L.aop, dd, t4, 128);
+      else
+        rows(N - 1 - w0, an, coln);
+    }
     const int xb0 = L.tb, xb1 = L.tb + 2 * d, xrt = L.rt;
     for (int it = w0, u = 0; it < N; it += NW, ++u) {
       const int n = N - 1 - it;
       const int4 pl = E.plan[(long)n * (Kc + 1) + 1 + kch];
+      if (DNS) {
+        cp_async_wait_all();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // A_n (and A_c) staged; the other buffer free
+        if (it + NW < N) stage_block(E.A + (long)(n - NW) * dd, L.aop + ((u + 1) & 1) * dd, dd, t4, 128);
+      } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) a[w] = an[w], col[w] = coln[w];
-      if (it + NW < N) rows(n - NW, an, coln);
+        for (int w = 0; w < W; ++w) a[w] = an[w], col[w] = coln[w];
+        if (it + NW < N) rows(n - NW, an, coln);
+      }
       const int slot = u % WR;
       long long* trc = E.trace ? E.trace + (((long)g * 8 + wi) * N + it) * 4 : nullptr;
       if (trc && t4 == 0) trc[0] = clock64();
@@ -790,7 +894,10 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
       if (t4 == 0) cl_arrive_relaxed(cl_map(&wempty[wi * WR + slot], 0));
-      x4_chain<W>(1, ix, d, top, cur, a, col, ac, accol, pl.x, pl.y, xb0, xb1, xrt, t4);
+      if (DNS)
+        x4_chain_dense(1, ix, d, top, cur, L.aop + (u & 1) * dd, L.aop + 2 * dd, pl.x, pl.y, xb0, xb1, xrt, t4);
+      else
+        x4_chain<W>(1, ix, d, top, cur, a, col, ac, accol, pl.x, pl.y, xb0, xb1, xrt, t4);
       if (trc && t4 == 0) trc[2] = clock64();
       // hand D_k to the dot warp
       const int b = u % WR;
@@ -842,22 +949,32 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN) lpsi |= 1u << si;
     }
     if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
-    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+    if (DNS)
+      stage_block(E.A + (long)(N - 1) * dd, L.aop, dd, tl, 64);
+    else
+      load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     team_sync(tm.id);
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
       const int4 pl = pln;
+      if (DNS) {
+        cp_async_wait_all();
+        team_sync(tm.id);
+        if (n > 0) stage_block(E.A + (long)(n - 1) * dd, L.aop + ((it + 1) & 1) * dd, dd, tl, 64);
+      } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-      if (n > 0) {
-        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
-        pln = E.plan[(long)(n - 1) * (Kc + 1)];
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+        if (n > 0) load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
       }
+      if (n > 0) pln = E.plan[(long)(n - 1) * (Kc + 1)];
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
       long long* trc = E.trace ? E.trace + (((long)g * 8 + 7) * N + it) * 4 : nullptr;
       if (trc && tl == 0) trc[0] = clock64();
-      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (DNS)
+        team_chain_dense(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      else
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[1] = clock64();
       const int w0 = it % NW, u = it / NW, wslot = u % WR;
       for (int k = 0; k < Kc; ++k)  // the workers' slots are free (they took psi of step it - WR * NW)
@@ -914,7 +1031,10 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       cur[0][0] = v;
     }
     team_sync(tm.id);
-    load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+    if (DNS)
+      stage_block(E.A + (long)(N - 1) * dd, L.aop, dd, tl, 64);
+    else
+      load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
@@ -935,13 +1055,22 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       }
       if (n == 0) break;
       const int4 pl = pln;
+      if (DNS) {
+        cp_async_wait_all();
+        team_sync(tm.id);
+        stage_block(E.A + (long)(n - 1) * dd, L.aop + ((it + 1) & 1) * dd, dd, tl, 64);
+      } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-      load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
+        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+      }
       pln = E.plan[(long)(n - 1) * (Kc + 1)];
       const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
       team_sync(tm.id);
-      team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      if (DNS)
+        team_chain_dense(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
+      else
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[2] = clock64();
       if (needs_psi) {  // source at psi_{n-1} (src/costs.py:341-353), formed by the source warp
         mb_wait(&sfull[slot], use & 1);
@@ -988,16 +1117,18 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
   cl_sync();  // no CTA leaves while its shared memory may still be addressed remotely
 }
 
-extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars) {
-  return ws_layout(d, nteams, I, Wp, extra_bars).words;
+extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars, int dense) {
+  return ws_layout(d, nteams, I, Wp, extra_bars, dense).words;
 }
 
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl) {
   (void)rpl;
+  if (W == 0)  // dense rows: forward and cluster backward only
+    return backward == 2 ? (void*)lg_k_wsc_backward<1, 1> : (backward ? nullptr : (void*)lg_k_ws_forward<1, 1>);
 #define LG_WS(W_)                                                                               \
   if (W == W_)                                                                                  \
-    return backward == 2 ? (void*)lg_k_wsc_backward<W_>                                         \
-                         : (backward ? (void*)lg_k_ws_backward<W_> : (void*)lg_k_ws_forward<W_>);
+    return backward == 2 ? (void*)lg_k_wsc_backward<W_, 0>                                      \
+                         : (backward ? (void*)lg_k_ws_backward<W_> : (void*)lg_k_ws_forward<W_, 0>);
   LG_WS(1) LG_WS(2) LG_WS(3) LG_WS(4) LG_WS(5) LG_WS(6) LG_WS(7) LG_WS(8) LG_WS(9)
 #undef LG_WS
   return nullptr;

@@ -55,10 +55,11 @@ def _states(rng, k, d):
 
 
 def _case(kind, seed=7, n_steps=6, kc=3):
-    """kind: 'ws' (sparse d=48), 'cl' (sparse d=320), 'cta' (dense d=24), 'dense' (dense d=600)."""
+    """kind: 'ws' (sparse d=48), 'wsdense' (dense d=40), 'cl' (sparse d=320), 'cta' (dense d=24, engine
+    forced), 'dense' (dense d=600)."""
     rng = np.random.default_rng(seed)
-    d = {"ws": 48, "cl": 320, "cta": 24, "dense": 600}[kind]
-    dense = kind in ("cta", "dense")
+    d = {"ws": 48, "wsdense": 40, "cl": 320, "cta": 24, "dense": 600}[kind]
+    dense = kind in ("wsdense", "cta", "dense")
     if dense:
         hs = _herm_sparse(rng, d, range(d), 1.0 / d)
         hc = [_herm_sparse(rng, d, range(d), 0.3 / d) for _ in range(kc)]
@@ -118,7 +119,14 @@ def _oracle(c, kinds, amps):
     return O.composite_grad(p, amps, c["dt"], terms), O.composite_cost(p, amps, c["dt"], terms)
 
 
-ENGINES = ["ws", "cl", "cta", "dense"]
+ENGINES = ["ws", "wsdense", "cl", "cta", "dense"]
+
+
+@pytest.fixture(autouse=True)
+def _force_engine(request, monkeypatch):
+    """The 'cta' cases force the single-CTA engine (small dense problems default to the ws engine)."""
+    if "engine" in request.fixturenames and request.getfixturevalue("engine") == "cta":
+        monkeypatch.setenv("LG_ENGINE", "cta")
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -134,7 +142,7 @@ def test_all_kinds_three_channels(engine):
     assert abs(composite_cost(prob, a, terms) - cc) <= 1e-12
     npb = NativeProblem(prob, terms, prob.initial_state, prob.basis)
     name = npb._lib.lg_engine_name(npb.handle).decode()
-    assert name.startswith({"ws": "ws", "cl": "cluster", "cta": "cta", "dense": "dense"}[engine]), name
+    assert name.startswith({"ws": "ws", "wsdense": "ws", "cl": "cluster", "cta": "cta", "dense": "dense"}[engine]), name
 
 
 @pytest.mark.parametrize("engine", ENGINES)
