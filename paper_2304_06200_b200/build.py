@@ -33,6 +33,7 @@ UNITS = {
     "lg_dense.cu": [],
     "lg_sweep_ws.cu": [],
     "lg_sweep_cl.cu": [],
+    **{f"lg_sweep_cl_w{w}.cu": [] for w in range(3, 10)},
 }
 
 
@@ -55,9 +56,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
 
+    headers = [s for s in _sources() if not s.endswith(".cu")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
     def compile_unit(item):
         unit, flags = item
         obj = os.path.join(OUT, unit.replace(".cu", ".o"))
+        src = os.path.join(SRC, unit)
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_header)):
+            return unit, obj, None
         cmd = [NVCC, *COMMON, *flags, "-c", os.path.join(SRC, unit), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(os.path.join(OUT, unit + ".ptxas.log"), "w") as fh:
@@ -67,6 +75,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     with ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
         for unit, obj, r in ex.map(compile_unit, UNITS.items()):
+            if r is None:  # up to date
+                objs.append(obj)
+                continue
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed for {unit}")

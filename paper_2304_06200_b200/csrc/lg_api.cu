@@ -122,8 +122,8 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     return LG_OK;
   };
   if (p->engine == 5) {
-    fwd = lg_cl_kernel(0, p->W, p->cl_maxc);
-    bwd = lg_cl_kernel(1, p->W, p->cl_maxc);
+    fwd = lg_cl_kernel(0, p->W, p->cl_maxc, p->cl_small);
+    bwd = lg_cl_kernel(1, p->W, p->cl_maxc, p->cl_small);
   }
   if (p->n_groups > 0) rc = p->engine == 5 ? cl_launch(fwd, false) : launch(fwd, grid, block, eargs, fsm, p->stream, p->multi);
   if (rc) return rc;

@@ -190,24 +190,46 @@ bool configure_cl(lg_problem* p, int smem_optin) {
     R = (int)((d + CS - 1) / CS);
   }
   if (R > 640 || R < H || H > 120) return false;
+  std::vector<int> gset, gt0, gnT;
+  for (int s = 0; s < 2; ++s) {
+    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
+    for (int a2 = lo; a2 < hi; ++a2) gset.push_back(s), gt0.push_back(p->set_t0[s] + a2), gnT.push_back(1);
+  }
+  if (gset.empty() || gset.size() > 64) return false;
+  // Ghost-zone blocks: Q Taylor terms per cluster exchange.  Each CTA also
+  // computes E rows beyond its own rows on both sides (E >= (Q-1)H, a multiple
+  // of 8 so the own rows keep their bank-conflict-free 8-row phase groups) and
+  // receives a halo of E + H rows, so one cluster barrier serves Q terms.  Pays
+  // off when the barrier (~500 cycles) dominates a term, i.e. few rows per CTA.
+  // Largest Q <= 6 whose CTAs still let every trajectory's cluster be resident at
+  // once (more threads per CTA can halve the CTAs per SM and add a second wave).
+  auto ext = [&](int q) { return q > 1 ? ((q - 1) * H + 7) / 8 * 8 : 0; };
+  int Qmax = R <= 200 ? 6 : 1;
+  if (const char* fq = std::getenv("LG_CL_Q")) Qmax = std::max(1, std::atoi(fq));
+  while (Qmax > 1 && (ext(Qmax) + H > R || R + 2 * ext(Qmax) > 640)) --Qmax;
   const long cap = std::min(smem_optin, 227 * 1024);
-  const int words = lg_cl_smem_words(R, H, cmax, p->W, 0);
-  if ((long)words * 16 > cap) return false;
-  int words_b = lg_cl_smem_words(R, H, cmax, p->W, p->Kc * p->Wc);
-  const bool acs = (long)words_b * 16 <= cap && !std::getenv("LG_CL_NOACS");
-  if (!acs) words_b = words;
-  void* f0 = lg_cl_kernel(0, p->W, maxc);
-  void* f1 = lg_cl_kernel(1, p->W, maxc);
-  if (!f0 || !f1) return false;
-  if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, words * 16) != cudaSuccess) return false;
-  if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) != cudaSuccess) return false;
-  for (void* f : {f0, f1})
-    if (CS > 8 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
-  {
+  int Q = 0, E = 0, words = 0, words_b = 0, small = 0, best_ncl = -1;
+  bool acs = false;
+  for (int q = Qmax; q >= 1; --q) {
+    const int e = ext(q), thr = 32 * ((R + 2 * e + 31) / 32);
+    const int w0 = lg_cl_smem_words(R, H, q, e, cmax, p->W, 0);
+    if ((long)w0 * 16 > cap) continue;
+    int wb = lg_cl_smem_words(R, H, q, e, cmax, p->W, p->Kc * p->Wc);
+    const bool a2 = (long)wb * 16 <= cap && !std::getenv("LG_CL_NOACS");
+    if (!a2) wb = w0;
+    const int sm2 = thr <= 256 && !std::getenv("LG_CL_NOSMALL");
+    void* f0 = lg_cl_kernel(0, p->W, maxc, sm2);
+    void* f1 = lg_cl_kernel(1, p->W, maxc, sm2);
+    if (!f0 || !f1) return false;
+    if (cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, w0 * 16) != cudaSuccess) return false;
+    if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, wb * 16) != cudaSuccess) return false;
+    for (void* f : {f0, f1})
+      if (CS > 8 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return false;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(32 * ((R + 31) / 32));
-    cfg.dynamicSmemBytes = words_b * 16;
+    cfg.blockDim = dim3(thr);
+    cfg.dynamicSmemBytes = wb * 16;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CS;
@@ -216,17 +238,23 @@ bool configure_cl(lg_problem* p, int smem_optin) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, f1, &cfg) != cudaSuccess || ncl < 1) {
+    if (cudaOccupancyMaxActiveClusters(&ncl, f1, &cfg) != cudaSuccess) {
       cudaGetLastError();
-      return false;
+      ncl = 0;
     }
+    if (ncl < 1) continue;
+    if (std::min(ncl, (int)gset.size()) > std::min(best_ncl, (int)gset.size())) {
+      best_ncl = ncl;
+      Q = q, E = e, words = w0, words_b = wb, small = sm2, acs = a2;
+    }
+    if (ncl >= (int)gset.size()) break;
   }
-  std::vector<int> gset, gt0, gnT;
-  for (int s = 0; s < 2; ++s) {
-    const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
-    for (int a2 = lo; a2 < hi; ++a2) gset.push_back(s), gt0.push_back(p->set_t0[s] + a2), gnT.push_back(1);
-  }
-  if (gset.empty() || gset.size() > 64) return false;
+  if (Q == 0) return false;
+  if (cudaFuncSetAttribute(lg_cl_kernel(0, p->W, maxc, small), cudaFuncAttributeMaxDynamicSharedMemorySize, words * 16) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(lg_cl_kernel(1, p->W, maxc, small), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           words_b * 16) != cudaSuccess)
+    return false;
   // renumbered column tables
   std::vector<int> cp((size_t)p->W * d), acp((size_t)p->Kc * p->Wc * d);
   for (long i2 = 0; i2 < d; ++i2) {
@@ -256,12 +284,15 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_CS = CS;
   p->cl_R = R;
   p->cl_H = H;
+  p->cl_Q = Q;
+  p->cl_E = E;
+  p->cl_small = small;
   p->cl_maxc = maxc;
   p->cl_smem = words * 16;
   p->cl_smem_b = words_b * 16;
   p->cl_acs = acs ? 1 : 0;
   p->cta_Imax = Imax;
-  p->threads = 32 * ((R + 31) / 32);
+  p->threads = 32 * ((R + 2 * E + 31) / 32);
   p->n_slabs = 1;
   p->grp_set = gset;
   p->grp_t0 = gt0;

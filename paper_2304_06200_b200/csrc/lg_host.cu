@@ -341,6 +341,8 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.trace = nullptr;
   E.cl_R = p->cl_R;
   E.cl_H = p->cl_H;
+  E.cl_Q = p->cl_Q;
+  E.cl_E = p->cl_E;
   E.cl_acs = 0;
   E.ws_nw = p->ws_nw;
   E.dense_rows = (p->dense && p->W == p->d && p->Wc == p->d) ? 1 : 0;

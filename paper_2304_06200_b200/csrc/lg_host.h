@@ -32,8 +32,8 @@ extern "C" void* lg_gather_kernel();
 extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 extern "C" void* lg_zgemm_kernel();
 extern "C" void* lg_taylor_epi_kernel();
-extern "C" void* lg_cl_kernel(int backward, int W, int maxc);
-extern "C" int lg_cl_smem_words(int R, int H, int cmax, int W, int acw);
+extern "C" void* lg_cl_kernel(int backward, int W, int maxc, int small);
+extern "C" int lg_cl_smem_words(int R, int H, int Q, int E, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
 extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars, int dense);
 extern "C" void* lg_dense_form_kernel();
@@ -145,7 +145,7 @@ struct lg_problem {
   double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
   size_t splitws_cap = 0;
   // cluster engine
-  int cl_CS = 0, cl_R = 0, cl_H = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
+  int cl_CS = 0, cl_R = 0, cl_H = 0, cl_Q = 1, cl_E = 0, cl_small = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
   unsigned char* d_cl_slot = nullptr;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;

@@ -1,0 +1,4 @@
+// Cluster sweep engine instantiations for ELL width 4 (see lg_sweep_cl.cuh).
+#include "lg_sweep_cl.cuh"
+
+LG_CL_KERNELS(4)

@@ -94,7 +94,8 @@ struct LgEngineArgs {
   const double2* trsum;     // [n_specs][N] trace sums (GATE_RUN), filled between sweeps
   long long* trace;         // optional: per-team clock64 trace [group][team][N][4] (LG_TRACE)
   // cluster engine (lg_sweep_cl.cu): RCM renumbering of the rows
-  int cl_R, cl_H;           // rows per CTA, halo width (bandwidth of the renumbered pattern)
+  int cl_R, cl_H;           // rows per CTA, bandwidth of the renumbered pattern
+  int cl_Q, cl_E;           // Taylor terms per cluster exchange; ghost rows computed beyond the own rows per side
   int cl_acs;               // backward stages the control-generator rows in shared memory
   int ws_nw;                // ws cluster backward: derivative workers per control channel
   int dense_rows;           // every operator row stores all d columns in order (dense H): slot w == column w
