@@ -6,8 +6,15 @@
 // kind), with the Taylor scale-and-accumulate fused into the epilogue:
 //     t = (A X) (sgn / (s j));  cur += t;  T_out = last ? cur : t.
 // A is stored planar (Ar, Ai), column-major; X / cur / T are interleaved
-// double2, column-major (column = one state vector).  The complex product is
-// four real MMAs per fragment pair: Yr += Ar Xr + Ai (-Xi), Yi += Ar Xi + Ai Xr.
+// double2, column-major (column = one state vector).  The complex product uses
+// three real MMAs per fragment pair (the 3M / Gauss scheme of ZGEMM3M):
+//     T1 += Ar Xr,  T2 += Ai Xi,  T3 += (Ar + Ai)(Xr + Xi);
+//     Yr = T1 - T2,  Yi = T3 - T1 - T2,
+// with the operand sums formed from the fragments already in registers, so the
+// tensor pipe does 3/4 of the 4M work at the same operand traffic.  (Norm-wise
+// error of 3M is a small multiple of the 4M bound -- Higham, "Stability of a
+// method for multiplying complex matrices with three real matrix
+// multiplications" -- far inside the parity tolerances.)
 // An operand may be the concatenation of two segments (the aux embedding's
 // top block [A | A_c] [top; bottom], src/derivatives.py:154-164).
 #include <cuda_runtime.h>
@@ -44,11 +51,13 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int M = G.M, C = G.C;
-  double yr[2][2][2], yi[2][2][2];
+  double t1[2][2][2], t2[2][2][2], t3[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) yr[a][b][0] = yr[a][b][1] = yi[a][b][0] = yi[a][b][1] = 0.0;
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) t1[a][b][v] = t2[a][b][v] = t3[a][b][v] = 0.0;
 
   // flattened k-tiles over the segments; this CTA's slice [t_lo, t_hi)
   int tiles0 = (G.seg[0].K + BK - 1) / BK;
@@ -112,42 +121,50 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       const int ka = kk + (lane & 3);
-      double ar[2], ai[2], xr[2], xi[2], nxi[2];
+      double ar[2], ai[2], sa[2], xr[2], xi[2], sx[2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int m = warp * 16 + mt * 8 + (lane >> 2);
         ar[mt] = sAr[buf][ka][m];
         ai[mt] = sAi[buf][ka][m];
+        sa[mt] = ar[mt] + ai[mt];
       }
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int n = nt * 8 + (lane >> 2);
         xr[nt] = sXr[buf][ka][n];
         xi[nt] = sXi[buf][ka][n];
-        nxi[nt] = -xi[nt];
+        sx[nt] = xr[nt] + xi[nt];
       }
-      // all Ar products first, then all Ai products: 8 independent DMMAs separate the two
-      // updates of an accumulator (back-to-back they stall on the DMMA latency)
+      // 12 independent DMMAs per k-step: each accumulator is updated once per step
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma(yr[mt][nt][0], yr[mt][nt][1], ar[mt], xr[nt]);
-          dmma(yi[mt][nt][0], yi[mt][nt][1], ar[mt], xi[nt]);
-        }
+        for (int nt = 0; nt < 2; ++nt) dmma(t1[mt][nt][0], t1[mt][nt][1], ar[mt], xr[nt]);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma(yr[mt][nt][0], yr[mt][nt][1], ai[mt], nxi[nt]);
-          dmma(yi[mt][nt][0], yi[mt][nt][1], ai[mt], xr[nt]);
-        }
+        for (int nt = 0; nt < 2; ++nt) dmma(t2[mt][nt][0], t2[mt][nt][1], ai[mt], xi[nt]);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma(t3[mt][nt][0], t3[mt][nt][1], sa[mt], sx[nt]);
     }
     if (t + 1 < total) {
       __syncthreads();  // everyone done reading sX[buf ^ 1] of tile t - 1
       store_x(buf ^ 1, xreg);
     }
   }
+  double yr[2][2][2], yi[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        yr[a][b][v] = t1[a][b][v] - t2[a][b][v];
+        yi[a][b][v] = (t3[a][b][v] - t1[a][b][v]) - t2[a][b][v];
+      }
   if (G.ksplit > 1) {  // raw partial product of this k-slice
     double2* P = G.partial + (long)blockIdx.z * M * C;
 #pragma unroll
