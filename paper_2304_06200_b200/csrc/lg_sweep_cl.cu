@@ -12,9 +12,7 @@ extern "C" void* lg_cl_kernel_w9(int backward, int maxc, int small);
 
 // acw = Kc * Wc when the backward kernel stages the control-generator rows, else 0.
 extern "C" int lg_cl_smem_words(int R, int H, int Q, int E, int cmax, int W, int acw) {
-  const int T = 32 * ((R + 2 * E + 31) / 32);
-  return 16 * 32 + 16 * 16 + 72 + (Q > 1 ? 4 : 2) * cmax * (R + 2 * (E + H)) + ((W + 3) / 4 * T + 3) / 4 + acw * T +
-         (acw * T + 3) / 4;
+  return lg_cl_mb_word(R, H, Q, E, cmax, W, acw) + 1;  // + the two exchange mbarriers
 }
 
 // small != 0: the <= 256-thread variant (see ClRegs).

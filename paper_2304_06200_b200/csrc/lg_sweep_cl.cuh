@@ -48,6 +48,11 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
   return v;
 }
 __device__ __forceinline__ unsigned smaddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cl_map_u(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
 __device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
   unsigned r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smaddr(p)), "r"(rank));
@@ -55,6 +60,26 @@ __device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
 }
 __device__ __forceinline__ void cl_st(unsigned addr, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+// Halo push of a block's last term: st.async into the neighbour's window, counted on
+// the neighbour's mbarrier of that buffer (complete_tx) -- no release fence.
+__device__ __forceinline__ void cl_st_async(unsigned addr, double2 v, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smaddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mb_arm(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smaddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smaddr(b)),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -86,6 +111,8 @@ struct Cl {
   int Cmax, Cst, Wc;
   int acs, accs;                        // staged control rows: double2 [Kc][Wc][T] and int [Kc][Wc][T] (-1: not staged)
   int cols;                             // packed slot columns, unsigned [(W+3)/4][T]
+  int mb;                               // two mbarriers (exchange buffers tb0 / tb1), 8-byte words after the layout
+  mutable unsigned ph;                  // parity bits of the next phase of mb[0], mb[1]
 };
 
 // SMALL: the CTA has <= 256 threads (few rows per CTA, latency-bound), so the
@@ -111,6 +138,36 @@ __device__ __forceinline__ void put(const Cl& c, int buf, int colo, double2 v) {
   cl_sm[off + c.H + c.li] = v;
   if (oi < c.HW && c.rank > 0) cl_st(cl_map(&cl_sm[off + c.R + c.HW + oi], c.rank - 1), v);
   if (oi >= c.R - c.HW && c.rank + 1 < c.CS) cl_st(cl_map(&cl_sm[off + oi - c.R + c.HW], c.rank + 1), v);
+}
+__device__ __forceinline__ unsigned long long* cl_mb(const Cl& c, int k) {
+  return reinterpret_cast<unsigned long long*>(cl_sm + c.mb) + k;
+}
+// Same for a block's last term inside a chain: the halo rows travel by st.async and are
+// counted on the neighbour's mbarrier of buffer yi (see exchange_begin / exchange_end).
+__device__ __forceinline__ void put_async(const Cl& c, int buf, int yi, int colo, double2 v) {
+  const int off = buf + colo * c.WIN, oi = c.li - c.E;
+  cl_sm[off + c.H + c.li] = v;
+  const unsigned mb = smaddr(cl_mb(c, yi));
+  if (oi < c.HW && c.rank > 0)
+    cl_st_async(cl_map(&cl_sm[off + c.R + c.HW + oi], c.rank - 1), v, cl_map_u(mb, c.rank - 1));
+  if (oi >= c.R - c.HW && c.rank + 1 < c.CS)
+    cl_st_async(cl_map(&cl_sm[off + oi - c.R + c.HW], c.rank + 1), v, cl_map_u(mb, c.rank + 1));
+}
+// Block exchange over the neighbour-only mbarriers (replaces one cluster barrier per
+// block).  Buffer yi's mbarrier is armed (one arrival + the expected halo bytes) when
+// a block that writes yi starts; neighbours' pushes may land before the arm (the
+// transaction count then runs negative within the phase).  The block ends with a CTA
+// barrier (own rows) and the wait for the halo bytes.  Write-after-read on the two
+// exchange buffers needs no handshake: a neighbour overwrites buffer yi only after
+// receiving this CTA's halo of the following block, i.e. after this CTA's reads of yi.
+__device__ __forceinline__ void exchange_begin(const Cl& c, int yi, int C) {
+  if (threadIdx.x == 0)
+    mb_arm(cl_mb(c, yi), 16u * (unsigned)(c.HW * C) * ((c.rank > 0 ? 1u : 0u) + (c.rank + 1 < c.CS ? 1u : 0u)));
+}
+__device__ __forceinline__ void exchange_end(const Cl& c, int yi) {
+  __syncthreads();
+  mb_wait(cl_mb(c, yi), (c.ph >> yi) & 1u);
+  c.ph ^= 1u << yi;
 }
 
 // Cluster-wide deterministic sum of nv values (per thread partials).
@@ -148,7 +205,7 @@ __device__ void cl_reduce(const Cl& c, double2 (&v)[NV], int nv) {
 // every thread (own and ghost rows) stores its term locally.
 template <int W, int MAXC, bool SMALL>
 __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, SMALL>& R, int C, int mode, int G,
-                                         int X, int Y, double r, bool last, bool fin) {
+                                         int X, int Y, double r, bool last, bool fin, int yi) {
 #pragma unroll
   for (int q = 0; q < MAXC; ++q) {
     if (q >= C) break;
@@ -188,7 +245,7 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
     const double2 tt = make_double2((p.x + pq.x) * r, (p.y + pq.y) * r);
     R.cur[q] = cadd(R.cur[q], tt);
     if (fin) {
-      if (c.slot) put(c, Y, q, last ? R.cur[q] : tt);
+      if (c.slot) put_async(c, Y, yi, q, last ? R.cur[q] : tt);
     } else if (c.act) {
       cl_sm[Y + q * c.WIN + c.H + c.li] = tt;
     }
@@ -200,7 +257,7 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
 // the sub-term are issued before its first store.
 template <int W, int MAXC, int NC, int MODE>
 __device__ __forceinline__ void sub_term(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, true>& R, int X, int Y,
-                                         double r, bool last, bool fin) {
+                                         double r, bool last, bool fin, int yi) {
   double2 tt[NC];
   if (c.ex && (c.slot || !fin)) {
 #pragma unroll
@@ -241,7 +298,7 @@ __device__ __forceinline__ void sub_term(const LgEngineArgs& E, const Cl& c, ClR
   for (int q = 0; q < NC; ++q) {
     R.cur[q] = cadd(R.cur[q], tt[q]);
     if (fin) {
-      if (c.slot) put(c, Y, q, last ? R.cur[q] : tt[q]);
+      if (c.slot) put_async(c, Y, yi, q, last ? R.cur[q] : tt[q]);
     } else if (c.act) {
       cl_sm[Y + q * c.WIN + c.H + c.li] = tt[q];
     }
@@ -250,22 +307,24 @@ __device__ __forceinline__ void sub_term(const LgEngineArgs& E, const Cl& c, ClR
 
 template <int W, int MAXC, int NC, int MODE>
 __device__ __forceinline__ void chain_nc(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, true>& R, int m, int s) {
-  int X = c.tb0, Y = c.tb1;
+  int X = c.tb0, Y = c.tb1, yi = 1;
   for (int round = 0; round < s; ++round)
     for (int j0 = 1; j0 <= m; j0 += c.Q) {
       const int b = min(c.Q, m - j0 + 1);
+      exchange_begin(c, yi, NC);
       for (int t = 1; t <= b; ++t) {
         const int j = j0 + t - 1;
         const bool fin = t == b;
         const int src = t == 1 ? X : ((t & 1) ? c.tb2 : c.tb3);
         const int dst = fin ? Y : ((t & 1) ? c.tb3 : c.tb2);
-        sub_term<W, MAXC, NC, MODE>(E, c, R, src, dst, cl_sm[c.rt + j - 1].x, j == m, fin);
+        sub_term<W, MAXC, NC, MODE>(E, c, R, src, dst, cl_sm[c.rt + j - 1].x, j == m, fin, yi);
         if (!fin) __syncthreads();
       }
-      cl_sync();
+      exchange_end(c, yi);
       const int t_ = X;
       X = Y;
       Y = t_;
+      yi ^= 1;
     }
 }
 
@@ -283,30 +342,32 @@ __device__ __forceinline__ void chain(const LgEngineArgs& E, const Cl& c, ClRegs
         chain_nc<W, MAXC, n, 0>(E, c, R, m, s);                             \
       else if constexpr (n >= 2)                                            \
         chain_nc<W, MAXC, n, 1>(E, c, R, m, s);                             \
-      return;                                                               \
     }
     LG_NC(1) LG_NC(2) LG_NC(3) LG_NC(4) LG_NC(5) LG_NC(6) LG_NC(7) LG_NC(8)
 #undef LG_NC
-    return;
-  }
-  int X = c.tb0, Y = c.tb1;  // exchange buffers: block input, block output
+  } else {
+  int X = c.tb0, Y = c.tb1, yi = 1;  // exchange buffers: block input, block output
   for (int round = 0; round < s; ++round)
     for (int j0 = 1; j0 <= m; j0 += c.Q) {
       const int b = min(c.Q, m - j0 + 1);
+      exchange_begin(c, yi, C);
       for (int t = 1; t <= b; ++t) {
         const int j = j0 + t - 1;
         const bool fin = t == b;
         const int src = t == 1 ? X : ((t & 1) ? c.tb2 : c.tb3);
         const int dst = fin ? Y : ((t & 1) ? c.tb3 : c.tb2);
         const double r = cl_sm[c.rt + j - 1].x;
-        term_row<W, MAXC, SMALL>(E, c, R, C, mode, G, src, dst, r, j == m, fin);
+        term_row<W, MAXC, SMALL>(E, c, R, C, mode, G, src, dst, r, j == m, fin, yi);
         if (!fin) __syncthreads();  // sub-term visible to the CTA (ghost rows are local)
       }
-      cl_sync();  // Y (own rows + halos) complete everywhere; X free for the block after next
+      exchange_end(c, yi);  // Y (own rows + halos) complete here
       const int t_ = X;
       X = Y;
       Y = t_;
+      yi ^= 1;
     }
+  }
+  cl_sync();  // every CTA done reading its windows: the caller may stage the next chain's input
 }
 
 template <int W, int MAXC, bool SMALL>
@@ -380,6 +441,8 @@ __device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst, 
     c.accs = o;
   }
   c.st = c.nx = 0;
+  c.mb = lg_cl_mb_word(c.R, c.H, c.Q, c.E, Cmax, W, E.cl_acs ? E.Kc * E.Wc : 0);
+  c.ph = 0;
   return c;
 }
 
@@ -407,6 +470,11 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
   for (int q = threadIdx.x; q < (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    mb_init(cl_mb(c, 0), 1);
+    mb_init(cl_mb(c, 1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   cl_sync();
   const double2 psi0 = c.own ? E.psi0[(long)t0 * c.d + c.orig] : make_double2(0.0, 0.0);
   double2 psi = psi0;
@@ -486,6 +554,11 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
   for (int q = threadIdx.x; q < (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    mb_init(cl_mb(c, 0), 1);
+    mb_init(cl_mb(c, 1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   if (c.acs >= 0)
     for (int kw = 0; kw < Kc * E.Wc; ++kw) {
       cl_sm[c.acs + kw * c.T + c.li] = c.ex ? E.Ac[(long)kw * c.d + c.orig] : make_double2(0.0, 0.0);

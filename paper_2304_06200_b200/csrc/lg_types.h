@@ -8,6 +8,15 @@
 #define LG_MAX_SPECS 8
 #define LG_MAXW 64  // widest ELL row handled by the bit-exact row-sum path
 
+// Cluster engine (lg_sweep_cl.cuh) shared-memory layout, in 16-byte words, up to the word
+// holding the two exchange mbarriers (reduction scratch, 1/(s j) table, 2 or 4 window
+// buffers of cmax columns, packed slot columns, staged control rows acw = Kc * Wc).
+__host__ __device__ inline int lg_cl_mb_word(int R, int H, int Q, int E, int cmax, int W, int acw) {
+  const int T = 32 * ((R + 2 * E + 31) / 32);
+  return 16 * 32 + 16 * 16 + 72 + (Q > 1 ? 4 : 2) * cmax * (R + 2 * (E + H)) + ((W + 3) / 4 * T + 3) / 4 + acw * T +
+         (acw * T + 3) / 4;
+}
+
 // Cost kinds (src/costs.py:49-61)
 enum LgKind { LGK_STATE_INF = 0, LGK_STATE_PEN = 1, LGK_STATE_RUN = 2, LGK_GATE = 3, LGK_GATE_RUN = 4 };
 
