@@ -96,8 +96,8 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   int fsm = p->smem_bytes, bsm = p->smem_bytes;
   dim3 bblock = block;
   if (p->engine == 4) {
-    fwd = lg_ws_kernel(0, p->dense ? 0 : p->W, p->ws_rpl);
-    bwd = lg_ws_kernel(1, p->dense ? 0 : p->W, p->ws_rpl);
+    fwd = lg_ws_kernel(0, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl);
+    bwd = lg_ws_kernel(1, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl);
     fsm = p->ws_fwd_smem;
     bsm = p->ws_bwd_smem;
     bblock = dim3(p->ws_bwd_threads);
@@ -156,7 +156,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       ++g_launches;
-      cudaError_t e = cudaLaunchKernelExC(&cfg, lg_ws_kernel(2, p->dense ? 0 : p->W, p->ws_rpl), eargs);
+      cudaError_t e = cudaLaunchKernelExC(&cfg, lg_ws_kernel(2, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl), eargs);
       if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
     } else {
       rc = launch(bwd, grid, bblock, eargs, bsm, p->stream, p->multi);

@@ -201,10 +201,13 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   // of 8 so the own rows keep their bank-conflict-free 8-row phase groups) and
   // receives a halo of E + H rows, so one cluster barrier serves Q terms.  Pays
   // off when the barrier (~500 cycles) dominates a term, i.e. few rows per CTA.
-  // Largest Q <= 6 whose CTAs still let every trajectory's cluster be resident at
+  // Largest Q <= Qmax whose CTAs still let every trajectory's cluster be resident at
   // once (more threads per CTA can halve the CTAs per SM and add a second wave).
   auto ext = [&](int q) { return q > 1 ? ((q - 1) * H + 7) / 8 * 8 : 0; };
-  int Qmax = R <= 200 ? 6 : 1;
+  // Q fills one 8-row ghost group (E = 8 for H <= 8): with the mbarrier exchange a block
+  // boundary costs ~250 cycles, less than the extra ghost rows of a wider group (c3, H = 4:
+  // Q = 3 194 ms, Q = 6 201 ms).
+  int Qmax = R <= 200 ? std::max(1, std::min(6, 1 + ((H + 7) / 8 * 8) / H)) : 1;
   if (const char* fq = std::getenv("LG_CL_Q")) Qmax = std::max(1, std::atoi(fq));
   while (Qmax > 1 && (ext(Qmax) + H > R || R + 2 * ext(Qmax) > 640)) --Qmax;
   const long cap = std::min(smem_optin, 227 * 1024);
@@ -313,7 +316,7 @@ bool configure_ws(lg_problem* p, int smem_optin) {
   const int dns = p->dense ? 1 : 0;
   if (p->d > 64 || p->Kc > 6) return false;
   if (dns ? (p->dense_large || p->W != p->d || p->Wc != p->d) : (p->W > 9 || p->Wc > 2)) return false;
-  const int kw = dns ? 0 : p->W;
+  const int kw = dns ? -lg_ws_dense_width((int)p->d) : p->W;
   int nspec[2] = {0, 0};
   int Wp = 1;
   for (auto& s : p->specs) {

@@ -35,6 +35,7 @@ extern "C" void* lg_taylor_epi_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc, int small);
 extern "C" int lg_cl_smem_words(int R, int H, int Q, int E, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
+extern "C" int lg_ws_dense_width(int d);
 extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars, int dense);
 extern "C" void* lg_dense_form_kernel();
 extern "C" void* lg_dots_kernel();

@@ -214,6 +214,62 @@ __device__ __forceinline__ void team_chain_dense(const Team& tm, double2& cur, i
     j = last ? 1 : j + 1;
   }
 }
+// Same chain with the lane's operator row held in registers for the whole step (DM >= d
+// columns, zero beyond d; the term buffers' second column region is zero, so the x
+// broadcasts past d read zeros): per term only the d broadcast x loads go through the
+// shared-memory pipe instead of d row loads + d broadcasts.
+template <int DM>
+__device__ __forceinline__ void team_chain_dense_r(const Team& tm, double2& cur, int aop, int m, int s, double sgn,
+                                                   int tb0, int tb1, int rt) {
+  if (tm.tl < m) ws_sm[rt + tm.tl].x = sgn * (1.0 / (double)(s * (tm.tl + 1)));
+  tsync(tm);
+  const int total = m * s, d = tm.d, i = tm.tl;
+  double2 ar[DM];
+#pragma unroll
+  for (int w = 0; w < DM; ++w) ar[w] = (i < d && w < d) ? ws_sm[aop + w * d + i] : make_double2(0.0, 0.0);
+  int j = 1;
+  auto term = [&](int X, int Y) {
+    const double r = ws_sm[rt + j - 1].x;
+    const bool last = j == m;
+    if (i < d) {
+      double2 p[4], q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] = q[u] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < DM; ++w) cmac(p[w & 3], q[w & 3], ar[w], ws_sm[X + w]);
+      const double2 pp = cadd(cadd(p[0], p[1]), cadd(p[2], p[3]));
+      const double2 qq = cadd(cadd(q[0], q[1]), cadd(q[2], q[3]));
+      const double2 tt = make_double2((pp.x + qq.x) * r, (pp.y + qq.y) * r);
+      cur = cadd(cur, tt);
+      if (last)
+        ws_sm[Y + i] = cur;
+      else
+        ws_sm[Y + i] = tt;
+    }
+    tsync(tm);
+    j = last ? 1 : j + 1;
+  };
+  for (int t = 0; t < total; t += 2) {
+    term(tb0, tb1);
+    if (t + 1 == total) break;
+    term(tb1, tb0);
+  }
+}
+// Smallest instantiated register row width DM >= d with DM <= 2d (team_chain_dense_r reads
+// the zero region past d).
+extern "C" int lg_ws_dense_width(int d) {
+  return d <= 8 ? 8 : d <= 16 ? 16 : d <= 32 ? 32 : d <= 40 ? 40 : d <= 48 ? 48 : 64;
+}
+// Register rows up to 48 columns; wider rows would spill (255 registers), so they stay in
+// shared memory.
+template <int DM>
+__device__ __forceinline__ void team_chain_dense_w(const Team& tm, double2& cur, int aop, int m, int s, double sgn,
+                                                   int tb0, int tb1, int rt) {
+  if constexpr (DM <= 48)
+    team_chain_dense_r<DM>(tm, cur, aop, m, s, sgn, tb0, tb1, rt);
+  else
+    team_chain_dense(tm, cur, aop, m, s, sgn, tb0, tb1, rt);
+}
 // Dense derivative chain on the four-warp team: top = A x_top + A_c x_bottom, bottom = A x_bottom.
 __device__ __forceinline__ void x4_chain_dense(int bar_id, int i, int d, bool top, double2& cur, int aop, int acop,
                                                int m, int s, int tb0, int tb1, int rt, int tl) {
@@ -417,6 +473,7 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
   const int team = threadIdx.x / 64;
   const Team tm{team + 1, (int)threadIdx.x % 64, 64, d};
   stage_specs(E, L, set, trel, I, Wp, pcol);
+  for (int q = threadIdx.x; q < 2 * 4 * d; q += blockDim.x) ws_sm[L.tb + q] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     for (int j = 0; j < RING; ++j) {
       mb_init(&full[j], 64);
@@ -454,7 +511,7 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
       if (n + 1 < N) pln = E.plan[(long)(n + 1) * (E.Kc + 1)];
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
       if (DNS)
-        team_chain_dense(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+        team_chain_dense_w<W>(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
       else
         team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
       const int slot = n % RING, use = n / RING;
@@ -778,7 +835,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_ws_backward(const __grid_constant
 // (mbarrier complete_tx); workers free slots with relaxed remote arrives.
 constexpr int WR = 4;  // ring slots per worker (psi / lambda) and derivative hand-off depth
 template <int W, int DNS>
-__global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constant__ LgEngineArgs E) {
+__global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constant__ LgEngineArgs E) {
   const int d = E.d, Kc = E.Kc, N = E.N, NW = E.ws_nw, NWK = Kc * E.ws_nw, IM = E.cta_Imax, dd = d * d;
   const unsigned rank = cl_rank();
   const int g = blockIdx.x / (1 + IM + NWK);
@@ -812,6 +869,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
     n_lpsi += (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN);
   }
   stage_specs(E, L, set, trel, I, Wp, pcol);
+  for (int q = threadIdx.x; q < 4 * d; q += blockDim.x) ws_sm[L.tb + q] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     if (rank == 0) {
       for (int j = 0; j < RING; ++j) mb_init(&pempty[j], n_lpsi > 0 ? n_lpsi : 1);
@@ -972,7 +1030,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       long long* trc = E.trace ? E.trace + (((long)g * 8 + 7) * N + it) * 4 : nullptr;
       if (trc && tl == 0) trc[0] = clock64();
       if (DNS)
-        team_chain_dense(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
+        team_chain_dense_w<W>(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
       else
         team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[1] = clock64();
@@ -1068,7 +1126,7 @@ __global__ void __launch_bounds__(512, 1) lg_k_wsc_backward(const __grid_constan
       const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
       team_sync(tm.id);
       if (DNS)
-        team_chain_dense(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
+        team_chain_dense_w<W>(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
       else
         team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
       if (trc && tl == 0) trc[2] = clock64();
@@ -1121,10 +1179,13 @@ extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_ba
   return ws_layout(d, nteams, I, Wp, extra_bars, dense).words;
 }
 
+// W > 0: sparse ELL width.  W <= 0: dense rows, -W = register row width DM (lg_ws_dense_width).
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl) {
   (void)rpl;
-  if (W == 0)  // dense rows: forward and cluster backward only
-    return backward == 2 ? (void*)lg_k_wsc_backward<1, 1> : (backward ? nullptr : (void*)lg_k_ws_forward<1, 1>);
+#define LG_WSD(DM_) \
+  if (W == -DM_) return backward == 2 ? (void*)lg_k_wsc_backward<DM_, 1> : (backward ? nullptr : (void*)lg_k_ws_forward<DM_, 1>);
+  LG_WSD(8) LG_WSD(16) LG_WSD(32) LG_WSD(40) LG_WSD(48) LG_WSD(64)
+#undef LG_WSD
 #define LG_WS(W_)                                                                               \
   if (W == W_)                                                                                  \
     return backward == 2 ? (void*)lg_k_wsc_backward<W_, 0>                                      \
