@@ -311,6 +311,11 @@ class NativeProblem:
             self._lib.lg_problem_destroy(h)
             self.handle = None
 
+    @property
+    def engine(self) -> str:
+        """Sweep engine the library chose for this problem (lg_engine_name)."""
+        return self._lib.lg_engine_name(self.handle).decode()
+
     def grad(self, a: ControlField) -> GradientResult:
         amps = np.ascontiguousarray(a.amplitudes, np.float64)
         cost = C.c_double()

@@ -227,3 +227,36 @@ def test_c5_prefix_dense_dmma():
     a8 = ControlField(8, 1, float(z["dt"]), models.controls(105, 1000, 1, 1.0)[:8])
     t = NativeProblem(case.problem, case.terms, initial_states=case.problem.initial_state).plan_table(a8)
     _plans_equal(t, z)
+
+
+# ----------------------------------------------------------------------------- cluster-engine variants
+
+
+@pytest.mark.parametrize("size,q,nosmall", [(16, 1, 0), (16, 3, 0), (16, 6, 0), (8, 3, 0), (16, 3, 1), (8, 2, 1)])
+def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
+    """Every cluster-engine layout (cluster size, ghost-zone block length Q, SMALL or generic
+    kernels) against the golden c3 prefix and the plan-sensitive block-aux stress variant."""
+    monkeypatch.setenv("LG_CL_SIZE", str(size))
+    monkeypatch.setenv("LG_CL_Q", str(q))
+    if nosmall:
+        monkeypatch.setenv("LG_CL_NOSMALL", "1")
+    z = G.load("c3")
+    hs, hc = G.mats(z)
+    prob = ControlProblem(hs, tuple(hc), initial_state=z["psi0"])
+    a = ControlField(z["amps"].shape[0], 2, float(z["dt"]), z["amps"])
+    terms = [CostTerm(CostKind.STATE_INFIDELITY, 1.0, target_state=z["targets"])]
+    npb = NativeProblem(prob, terms, initial_states=z["psi0"])
+    _check(npb.grad(a), z["cost"], z["grad"])
+    assert npb.engine.startswith("cluster"), npb.engine
+    zs = G.sub(G.load("stress"), "s_block160")
+    hs, hc = G.mats(zs)
+    om = G.penalty(zs)
+    N, Kc = zs["amps"].shape
+    a = ControlField(N, Kc, float(zs["dt"]), zs["amps"])
+    prob = ControlProblem(hs, tuple(hc), initial_state=zs["psi0"], basis=zs["basis"])
+    terms = [CostTerm(CostKind.STATE_INFIDELITY, 0.7, target_state=zs["targets"]),
+             CostTerm(CostKind.STATE_PENALTY, 0.2, penalty_op=om),
+             CostTerm(CostKind.STATE_RUNNING_INFIDELITY, 0.4, target_state=zs["targets"])]
+    _check(NativeProblem(prob, terms, initial_states=zs["psi0"]).grad(a), zs["cost_state"], zs["grad_state"])
+    t = [CostTerm(CostKind.GATE_RUNNING_INFIDELITY, 1.0, target_images=zs["images"])]
+    _check(NativeProblem(prob, t, basis=zs["basis"]).grad(a), zs["cost_g3"], zs["grad_g3"])
