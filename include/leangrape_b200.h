@@ -80,6 +80,10 @@ typedef struct {
   const lg_cost_term* terms;
   int32_t device;
   int64_t shard_begin, shard_end;
+  /* Backend (src/derivatives.py:48-51): 0 SCALING_SQUARING (certified Taylor action),
+   * 1 DIAGONALIZATION (per-step eigenfactorisation, src/derivatives.py:228-275; dense
+   * operators, d <= 128). */
+  int32_t backend;
 } lg_problem_desc;
 
 typedef struct lg_problem lg_problem;

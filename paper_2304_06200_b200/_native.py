@@ -67,6 +67,7 @@ class lg_problem_desc(C.Structure):
         ("device", C.c_int32),
         ("shard_begin", C.c_int64),
         ("shard_end", C.c_int64),
+        ("backend", C.c_int32),
     ]
 
 

@@ -34,6 +34,7 @@ UNITS = {
     "lg_sweep_ws.cu": [],
     "lg_sweep_cl.cu": [],
     **{f"lg_sweep_cl_w{w}.cu": [] for w in range(3, 10)},
+    "lg_diag.cu": [],
 }
 
 
@@ -85,7 +86,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(r.stderr)
             objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcublas", "-lcusolver"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -5,7 +5,9 @@ Same names, argument meaning and error behaviour as ``leangrape.costs``:
 ``GradientResult``, ``composite_grad``, ``composite_cost``, ``c1/c2/c3_state_grad``,
 ``c1/c3_gate_grad``, ``forward_propagate``.  Every evaluation runs the
 sm_100a kernels through the C ABI (include/leangrape_b200.h); there is no CPU
-fallback and the DIAGONALIZATION backend raises.
+fallback.  Both backends run on the device: SCALING_SQUARING (the certified
+Taylor action) and DIAGONALIZATION (per-step eigenfactorisation, dense d <= 128,
+lg_diag.cu).
 
 K-state block extension (documented in DESIGN.md):
   * ``ControlProblem.initial_state`` may be ``(K, d)``: state terms are then the
@@ -26,7 +28,7 @@ from enum import Enum
 import numpy as np
 
 from . import _native
-from .sparse import DenseMatrix, is_hermitian, one_norm_host
+from .sparse import DenseMatrix, is_hermitian, one_norm_host, to_dense
 
 __all__ = [
     "Backend",
@@ -229,16 +231,17 @@ class NativeProblem:
 
     def __init__(self, problem: ControlProblem, terms, initial_states=None, basis=None, device: int = 0,
                  shard: tuple[int, int] | None = None):
-        if problem.backend is not Backend.SCALING_SQUARING:
-            raise NotImplementedError("only the SCALING_SQUARING backend runs on the device (no CPU fallback)")
+        diag = problem.backend is Backend.DIAGONALIZATION
         lib = _native.load()
         d = problem.dim
         keep = _Keep()
         desc = _native.lg_problem_desc()
-        desc.h_static = _matrix(problem.h_static, d, keep)
+        # DIAGONALIZATION factorises the dense step matrix (src/derivatives.py:228-230): dense operators
+        dn = (lambda m: DenseMatrix(to_dense(m))) if diag else (lambda m: m)
+        desc.h_static = _matrix(dn(problem.h_static), d, keep)
         ctrls = (_native.lg_matrix * len(problem.h_controls))()
         for k, h in enumerate(problem.h_controls):
-            ctrls[k] = _matrix(h, d, keep)
+            ctrls[k] = _matrix(dn(h), d, keep)
         keep.arr(ctrls)
         desc.n_channels = len(problem.h_controls)
         desc.h_controls = ctrls
@@ -296,6 +299,7 @@ class NativeProblem:
         desc.n_terms = len(terms)
         desc.terms = cterms
         desc.device = device
+        desc.backend = 1 if diag else 0
         if shard is not None:
             desc.shard_begin, desc.shard_end = shard
         h = C.c_void_p()

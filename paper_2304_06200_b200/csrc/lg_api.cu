@@ -496,6 +496,7 @@ int lg_plan_table(lg_problem* p, int64_t n_steps, double dt, const double* amps,
                   int32_t* aux_scaling) {
   int rc = check_field(p, n_steps, dt, amps);
   if (rc) return rc;
+  if (p->backend == 1) return fail(LG_UNSUPPORTED, "the DIAGONALIZATION backend has no Taylor plans");
   CK(cudaSetDevice(p->device));
   rc = ensure_N(p, n_steps);
   if (rc) return rc;

@@ -419,19 +419,19 @@ bool configure_cta(lg_problem* p, int nsm, int smem_optin) {
     const long threads = rl * cs;
     if (threads > (maxr == 1 ? 512 : 1024)) continue;
     int wreg = (p->W <= 9 && !(maxr == 2 && maxc == 2) && maxr <= 2 && maxc <= 2) ? p->W : 0;
-    if (std::getenv("LG_CTA_NOWREG")) wreg = 0;
+    if (std::getenv("LG_CTA_NOWREG") || p->backend == 1) wreg = 0;
     const long red_cap = (long)Imax * std::max(p->Kc, 1) * T + 1;
     long words = red_cap * (rl / 32) + red_cap + 64 + 2 * cstate * d + 2 * cmax * d;  // double2 units
     const long budget = std::min<long>(smem_optin, 227 * 1024) / 16;
     if (words > budget) continue;
     int mode = 0;
     const long a_words = (long)p->W * d + ((long)p->W * d + 1) / 2;
-    if (wreg == 0 && words + a_words <= budget && !std::getenv("LG_CTA_NOASMEM")) {
+    if (wreg == 0 && words + a_words <= budget && !std::getenv("LG_CTA_NOASMEM") && p->backend == 0) {
       mode |= 4;
       words += a_words;
     }
     const long ac_words = (long)p->Kc * p->Wc * d + ((long)p->Kc * p->Wc * d + 1) / 2;
-    if (words + ac_words <= budget && !std::getenv("LG_CTA_NOACSMEM")) {
+    if (words + ac_words <= budget && !std::getenv("LG_CTA_NOACSMEM") && p->backend == 0) {
       mode |= 8;
       words += ac_words;
     }
@@ -476,6 +476,10 @@ int configure(lg_problem* p) {
   const long d = p->d;
   const char* force = std::getenv("LG_ENGINE");
   const std::string fs = force ? force : "";
+  if (p->backend == 1) {  // DIAGONALIZATION: CTA engine, one dense operator application per propagator
+    if (configure_cta(p, nsm, smem_optin)) return LG_OK;
+    return fail(LG_UNSUPPORTED, "DIAGONALIZATION backend: problem does not fit the CTA engine");
+  }
   bool multi = d > 4096;
   if (fs == "multi") multi = true;
   if (fs == "single" || fs == "legacy") multi = false;

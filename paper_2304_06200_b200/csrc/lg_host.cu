@@ -197,6 +197,7 @@ int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_
 
 // Steps 1-2: generators, planner inputs, plans (all steps at once).
 int prepare_steps(lg_problem* p, long N, double dt, bool need_aux) {
+  if (p->backend == 1) return prepare_diag(p, N, dt, need_aux);
   p->mark(0);
   int rc = prepare_dt(p, dt);
   if (rc) return rc;
@@ -343,6 +344,9 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.cl_H = p->cl_H;
   E.cl_Q = p->cl_Q;
   E.cl_E = p->cl_E;
+  E.diag = p->backend == 1 ? 1 : 0;
+  E.diag_Ud = p->d_Ud;
+  E.diag_D = p->d_D;
   E.cl_acs = 0;
   E.ws_nw = p->ws_nw;
   E.dense_rows = (p->dense && p->W == p->d && p->Wc == p->d) ? 1 : 0;
@@ -466,6 +470,10 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
   }
   p->T_total = (int)(p->traj.size() / d);
   // sharding (multi-GPU): each set propagates only trajectories [shard_begin, shard_end) of itself
+  p->backend = D->backend;
+  if (p->backend < 0 || p->backend > 1) return fail(LG_INVALID_ARG, "unknown backend");
+  if (p->backend == 1 && (!p->dense || d > 128))
+    return fail(LG_UNSUPPORTED, "the DIAGONALIZATION backend runs dense operators with d <= 128 on the device");
   p->shard_b = D->shard_end > 0 ? D->shard_begin : 0;
   p->shard_e = D->shard_end > 0 ? D->shard_end : (1L << 40);
   for (int t = 0; t < D->n_terms; ++t) {

@@ -101,6 +101,8 @@ struct Spec {
   double2* d_tgt = nullptr;
 };
 
+void release_diag(lg_problem* p);  // lg_diag.cu
+
 }  // namespace lgi
 
 using lgi::DevMem;
@@ -198,11 +200,23 @@ struct lg_problem {
   long lastN = 0;
   bool own_stream = true;
   bool timing = false;
+  // DIAGONALIZATION backend (lg_diag.cu): per-step exact propagators and derivative operators
+  int backend = 0;                 // 0 scaling-and-squaring (Taylor), 1 diagonalization
+  DevMem diagmem;                  // per-N: U^dagger, D, eigen workspace
+  long diag_capN = 0;
+  bool diag_need_aux = false;
+  double2 *d_Ud = nullptr, *d_D = nullptr, *d_V = nullptr, *d_wk0 = nullptr, *d_wk1 = nullptr, *d_ph = nullptr;
+  double* d_w = nullptr;
+  int* d_info = nullptr;
+  void* cublas = nullptr;          // cublasHandle_t
+  void* cusolver = nullptr;        // cusolverDnHandle_t
+  const char* diag_solver = "";
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double phase_ms[4] = {0, 0, 0, 0};
   long timed_evals = 0;
 
   ~lg_problem() {
+    lgi::release_diag(this);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     nmem.release();
@@ -236,6 +250,7 @@ int prepare_dt(lg_problem* p, double dt);
 int ensure_N(lg_problem* p, long N);
 int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop = false);
 int prepare_steps(lg_problem* p, long N, double dt, bool need_aux);
+int prepare_diag(lg_problem* p, long N, double dt, bool need_aux);  // lg_diag.cu
 LgEngineArgs engine_args(lg_problem* p, long N);
 LgFinalArgs final_args(lg_problem* p, long N, const double2* ip, const double2* fin, const double* run,
                        const double2* trp, double* grad, double* cost);

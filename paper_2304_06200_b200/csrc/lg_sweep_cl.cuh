@@ -205,7 +205,12 @@ __device__ void cl_reduce(const Cl& c, double2 (&v)[NV], int nv) {
 // every thread (own and ghost rows) stores its term locally.
 template <int W, int MAXC, bool SMALL>
 __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, SMALL>& R, int C, int mode, int G,
-                                         int X, int Y, double r, bool last, bool fin, int yi) {
+                                         int X, int Y, double r, bool last, bool fin, int yi, int vt) {
+  // Ghost rows that fall out of the valid region after sub-term vt are stored as zeros: the
+  // ELL pad slots (value 0) of a valid row may point up to H + 7 rows away (cl_color_slots
+  // reuses another row's address), and garbage left to grow there could reach Inf (0 * Inf).
+  const int pos = c.H + c.li;
+  const bool keep = pos >= vt * c.H && pos < c.WIN - vt * c.H;
 #pragma unroll
   for (int q = 0; q < MAXC; ++q) {
     if (q >= C) break;
@@ -247,7 +252,7 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
     if (fin) {
       if (c.slot) put_async(c, Y, yi, q, last ? R.cur[q] : tt);
     } else if (c.act) {
-      cl_sm[Y + q * c.WIN + c.H + c.li] = tt;
+      cl_sm[Y + q * c.WIN + c.H + c.li] = keep ? tt : make_double2(0.0, 0.0);
     }
   }
 }
@@ -257,7 +262,9 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
 // the sub-term are issued before its first store.
 template <int W, int MAXC, int NC, int MODE>
 __device__ __forceinline__ void sub_term(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, true>& R, int X, int Y,
-                                         double r, bool last, bool fin, int yi) {
+                                         double r, bool last, bool fin, int yi, int vt) {
+  const int pos = c.H + c.li;  // see term_row
+  const bool keep = pos >= vt * c.H && pos < c.WIN - vt * c.H;
   double2 tt[NC];
   if (c.ex && (c.slot || !fin)) {
 #pragma unroll
@@ -300,7 +307,7 @@ __device__ __forceinline__ void sub_term(const LgEngineArgs& E, const Cl& c, ClR
     if (fin) {
       if (c.slot) put_async(c, Y, yi, q, last ? R.cur[q] : tt[q]);
     } else if (c.act) {
-      cl_sm[Y + q * c.WIN + c.H + c.li] = tt[q];
+      cl_sm[Y + q * c.WIN + c.H + c.li] = keep ? tt[q] : make_double2(0.0, 0.0);
     }
   }
 }
@@ -317,7 +324,7 @@ __device__ __forceinline__ void chain_nc(const LgEngineArgs& E, const Cl& c, ClR
         const bool fin = t == b;
         const int src = t == 1 ? X : ((t & 1) ? c.tb2 : c.tb3);
         const int dst = fin ? Y : ((t & 1) ? c.tb3 : c.tb2);
-        sub_term<W, MAXC, NC, MODE>(E, c, R, src, dst, cl_sm[c.rt + j - 1].x, j == m, fin, yi);
+        sub_term<W, MAXC, NC, MODE>(E, c, R, src, dst, cl_sm[c.rt + j - 1].x, j == m, fin, yi, t);
         if (!fin) __syncthreads();
       }
       exchange_end(c, yi);
@@ -357,7 +364,7 @@ __device__ __forceinline__ void chain(const LgEngineArgs& E, const Cl& c, ClRegs
         const int src = t == 1 ? X : ((t & 1) ? c.tb2 : c.tb3);
         const int dst = fin ? Y : ((t & 1) ? c.tb3 : c.tb2);
         const double r = cl_sm[c.rt + j - 1].x;
-        term_row<W, MAXC, SMALL>(E, c, R, C, mode, G, src, dst, r, j == m, fin, yi);
+        term_row<W, MAXC, SMALL>(E, c, R, C, mode, G, src, dst, r, j == m, fin, yi, t);
         if (!fin) __syncthreads();  // sub-term visible to the CTA (ghost rows are local)
       }
       exchange_end(c, yi);  // Y (own rows + halos) complete here
@@ -469,7 +476,10 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __
   Cl c = make_cl(E, cmax, cst, W);
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
-  for (int q = threadIdx.x; q < (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
+  // zero everything up to the end of the window buffers (pad gathers may read a few rows past a
+  // window edge, into the neighbouring column or the tables in front of tb0)
+  for (int q = threadIdx.x; q < c.tb0 + (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x)
+    cl_sm[q] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     mb_init(cl_mb(c, 0), 1);
     mb_init(cl_mb(c, 1), 1);
@@ -553,7 +563,10 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
   Cl c = make_cl(E, cmax, cst, W);
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
-  for (int q = threadIdx.x; q < (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x) cl_sm[c.tb0 + q] = make_double2(0.0, 0.0);
+  // zero everything up to the end of the window buffers (pad gathers may read a few rows past a
+  // window edge, into the neighbouring column or the tables in front of tb0)
+  for (int q = threadIdx.x; q < c.tb0 + (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x)
+    cl_sm[q] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     mb_init(cl_mb(c, 0), 1);
     mb_init(cl_mb(c, 1), 1);

@@ -75,6 +75,7 @@ struct Ctx {
   bool a_smem, ac_smem;
   bool dense;            // dense rows: slot w is column w (no index loads)
   const double2* astep;  // global A_n of the current step (global-A mode)
+  int n;                 // current step (DIAGONALIZATION operators)
   Lay L;
 };
 
@@ -107,9 +108,68 @@ __device__ __forceinline__ void cmac(double2& p, double2& q, double2 a, double2 
 // the term buffer so every term reads the same way; everything that does not
 // change from term to term (offsets, control rows, 1/(s j)) is hoisted.
 // Result: the cur registers of the owned (row, column)s.
+// DIAGONALIZATION backend (lg_diag.cu): the chain is one application of the step's exact
+// operator -- U_n (sgn > 0), U_n^dagger (sgn < 0), or for the aux tops dU_n/da_k acting on the
+// bottom input (src/derivatives.py:249-275).  Same staging and result registers as chain().
+template <int MAXR, int MAXC, int WREG>
+__device__ __forceinline__ void chain_diag(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int mode,
+                                           double sgn, int xin, const int* gch, int G) {
+  const LgEngineArgs& E = *c.E;
+  const int d = c.d, T = c.T;
+  const long dd = (long)d * d;
+  const int ntop = mode == 1 ? G * T : 0;
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = c.slot + q * c.cs;
+    const bool own = col < C, top = own && col < ntop;
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+      const int i = row_of(c, k);
+      double2 v = make_double2(0.0, 0.0);
+      if (own && i < d) {
+        if (mode == 0)
+          v = SMX(xin + col * d + i);
+        else if (!top)
+          v = SMX(xin + (col - ntop) * d + i);
+        SMX(c.L.tb0 + col * d + i) = v;
+      }
+      R.cur[q][k] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = c.slot + q * c.cs;
+    if (col >= C) continue;
+    const bool top = col < ntop;
+    if (mode == 1 && !top) continue;  // bottoms: not needed by the derivative
+    const double2* op = mode == 0 ? (sgn > 0.0 ? c.astep : E.diag_Ud + (long)c.n * dd)
+                                  : E.diag_D + ((long)c.n * E.Kc + gch[col / T]) * dd;
+    const int x = c.L.tb0 + (mode == 0 ? col : ntop + col % T) * d;
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+      const int i = row_of(c, k);
+      if (i >= d) continue;
+      double2 p0 = make_double2(0.0, 0.0), q0 = p0, p1 = p0, q1 = p0;
+      int w = 0;
+      for (; w + 2 <= d; w += 2) {
+        cmac(p0, q0, op[(long)w * d + i], SMX(x + w));
+        cmac(p1, q1, op[(long)(w + 1) * d + i], SMX(x + w + 1));
+      }
+      for (; w < d; ++w) cmac(p0, q0, op[(long)w * d + i], SMX(x + w));
+      R.cur[q][k] = make_double2((p0.x + q0.x) + (p1.x + q1.x), (p0.y + q0.y) + (p1.y + q1.y));
+    }
+  }
+  __syncthreads();
+}
+
 template <int MAXR, int MAXC, int WREG>
 __device__ __forceinline__ void chain(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int C, int mode, int m, int s,
                                       double sgn, int xin, const int* gch, int G) {
+  if (c.E->diag) {
+    chain_diag<MAXR, MAXC, WREG>(c, sm, R, C, mode, sgn, xin, gch, G);
+    return;
+  }
   const int d = c.d, T = c.T, Wc = c.Wc, W = c.W;
   const int ntop = mode == 1 ? G * T : 0;
   const int* smi = reinterpret_cast<const int*>(lg_smem);
@@ -273,6 +333,7 @@ __device__ void load_step(Ctx& c, double2* sm, Regs<MAXR, MAXC, WREG>& R, int n)
   const int d = c.d, W = c.W;
   const double2* src = E.A + (long)n * W * d;
   c.astep = src;
+  c.n = n;
   if (WREG > 0) {
 #pragma unroll
     for (int k = 0; k < MAXR; ++k) {

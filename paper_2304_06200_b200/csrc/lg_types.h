@@ -105,6 +105,11 @@ struct LgEngineArgs {
   // cluster engine (lg_sweep_cl.cu): RCM renumbering of the rows
   int cl_R, cl_H;           // rows per CTA, bandwidth of the renumbered pattern
   int cl_Q, cl_E;           // Taylor terms per cluster exchange; ghost rows computed beyond the own rows per side
+  // DIAGONALIZATION backend (CTA engine): A holds U_n = exp(-i H_n dt) column-major per step,
+  // diag_Ud U_n^dagger, diag_D [N][Kc] the derivative operators dU_n/da_k (src/derivatives.py:251-275)
+  int diag;
+  const double2* diag_Ud;
+  const double2* diag_D;
   int cl_acs;               // backward stages the control-generator rows in shared memory
   int ws_nw;                // ws cluster backward: derivative workers per control channel
   int dense_rows;           // every operator row stores all d columns in order (dense H): slot w == column w

@@ -402,6 +402,52 @@ def golden_stress():
     save("stress", **out)
 
 
+def golden_diag():
+    """The reference's DIAGONALIZATION backend (src/derivatives.py:228-275): every cost kind on a
+    dense d = 40 problem (c1's model), a CSR d = 24 and a CSR d = 60 problem, random states,
+    large amplitudes.  Sparse inputs stay CSR here: the reference densifies each step."""
+    out = {}
+    rng = np.random.default_rng(7171)
+    DIAG = derivatives.Backend.DIAGONALIZATION
+
+    def one(tag, h_s, ctrls, N, dt, amp, K, seed):
+        d = h_s.n_rows
+        amps = controls(seed, N, len(ctrls), amp)
+        a = costs.ControlField(N, len(ctrls), dt, amps)
+        psi0s = rand_states(rng, K, d)
+        phis = rand_states(rng, K, d)
+        om = sparse.build_csr_arrays(np.arange(d), np.arange(d), (np.arange(d) % 5).astype(np.complex128) / 5.0, d, d)
+        kw = dict(h_static=h_s, h_controls=tuple(ctrls), backend=DIAG)
+        mk = lambda h: [costs.CostTerm(costs.CostKind.STATE_INFIDELITY, 0.7, target_state=phis[h]),
+                        costs.CostTerm(costs.CostKind.STATE_PENALTY, 0.2, penalty_op=om),
+                        costs.CostTerm(costs.CostKind.STATE_RUNNING_INFIDELITY, 0.4, target_state=phis[h])]
+        cs, gs = ref_state_block(kw, a, list(psi0s), mk)
+        css = ref_cost_block(kw, a, list(psi0s), mk)
+        q, _ = np.linalg.qr(rng.standard_normal((d, K)) + 1j * rng.standard_normal((d, K)))
+        basis = [q[:, h].copy() for h in range(K)]
+        u, _ = np.linalg.qr(rng.standard_normal((K, K)) + 1j * rng.standard_normal((K, K)))
+        images = [sum(u[j, h] * basis[j] for j in range(K)) for h in range(K)]
+        pr = costs.ControlProblem(h_s, tuple(ctrls), backend=DIAG)
+        cg1, gg1 = ref_gate_pass_subspace(pr, a, basis, images, running=False)
+        cg3, gg3 = ref_gate_pass_subspace(pr, a, basis, images, running=True)
+        print(f"diag {tag}: d={d} N={N} K={K} cost_state={cs:.6f} cost_g1={cg1:.6f}")
+        pay = mats_payload(h_s, ctrls)
+        out.update({f"{tag}__{k}": v for k, v in pay.items()})
+        out.update({f"{tag}__{k}": v for k, v in dict(
+            amps=amps, dt=dt, psi0=psi0s, targets=phis, pen_indptr=om.row_offsets, pen_indices=om.col_indices,
+            pen_data=om.values, basis=np.array(basis), images=np.array(images),
+            cost_state=cs, grad_state=gs, cost_state_only=css, cost_g1=cg1, grad_g1=gg1, cost_g3=cg3,
+            grad_g3=gg3).items()})
+
+    h_s, hx, _ = tc_ops(4, 10)
+    one("d_dense40", sparse.DenseMatrix(h_s.to_dense()), [sparse.DenseMatrix(hx.to_dense())], 40, 0.5, 1.0, 2, 401)
+    h_s, hx, hy = tc_ops(3, 8)
+    one("d_csr24", h_s, [hx, hy], 20, 0.5, 1.0, 3, 402)
+    h_s, hx, hy = tc_ops(3, 20)
+    one("d_csr60", h_s, [hx, hy], 16, 0.25, 1.0, 2, 403)
+    save("diag", **out)
+
+
 def golden_full_basis_check():
     """Restated subspace gate pass == reference c1/c3_gate_grad at K == d (bitwise)."""
     rng = np.random.default_rng(31)
@@ -467,6 +513,6 @@ def golden_expm():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["planner", "numpy_rules", "full_basis_check", "c1", "c2", "stress", "c3", "c4", "c5",
-                             "expm"]
+                             "expm", "diag"]
     for w in which:
         globals()["golden_" + w]()

@@ -246,7 +246,9 @@ def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
     a = ControlField(z["amps"].shape[0], 2, float(z["dt"]), z["amps"])
     terms = [CostTerm(CostKind.STATE_INFIDELITY, 1.0, target_state=z["targets"])]
     npb = NativeProblem(prob, terms, initial_states=z["psi0"])
-    _check(npb.grad(a), z["cost"], z["grad"])
+    for _ in range(4):  # repeated gradient and forward-only calls on one problem (intermittent-race guard)
+        _check(npb.grad(a), z["cost"], z["grad"])
+        assert abs(npb.cost(a) - float(z["cost"])) <= COST_TOL
     assert npb.engine.startswith("cluster"), npb.engine
     zs = G.sub(G.load("stress"), "s_block160")
     hs, hc = G.mats(zs)

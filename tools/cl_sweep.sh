@@ -1,3 +1,4 @@
-timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 120 python tools/run_eval.py c1 full 3 2>&1 | tail -2
-timeout 120 python tools/run_eval.py c2 full 5 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 120 python tools/run_eval.py c3 full 3 2>&1 | tail -2
+timeout 200 python tools/run_eval.py c4 400 2 2>&1 | tail -2
+TAG=default timeout 300 python tools/racecheck.py 30
