@@ -23,7 +23,8 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 16, BK = 16, SA = BM + 8, SX = BN + 1;
+constexpr int BM = 64, BK = 16, SA = BM + 8;
+extern __shared__ __align__(16) double zg_dsm[];
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -42,20 +43,24 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 
 
-// grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x 16 tile.
-extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
-  __shared__ __align__(16) double sAr[2][BK][SA];
-  __shared__ __align__(16) double sAi[2][BK][SA];
-  __shared__ double sXr[2][BK][SX];
-  __shared__ double sXi[2][BK][SX];
+// grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x BN tile,
+// BN = 8 NTT columns (NTT = 2 or 4: the wider tile halves the A-fragment loads per DMMA).
+// Dynamic shared memory: zgemm_smem_bytes(NTT).
+template <int NTT>
+__device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
+  constexpr int BN = 8 * NTT, SX = BN + 1;
+  auto sAr = reinterpret_cast<double(*)[BK][SA]>(zg_dsm);
+  auto sAi = reinterpret_cast<double(*)[BK][SA]>(zg_dsm + 2 * BK * SA);
+  auto sXr = reinterpret_cast<double(*)[BK][SX]>(zg_dsm + 4 * BK * SA);
+  auto sXi = reinterpret_cast<double(*)[BK][SX]>(zg_dsm + 4 * BK * SA + 2 * BK * SX);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int M = G.M, C = G.C;
-  double t1[2][2][2], t2[2][2][2], t3[2][2][2];
+  double t1[2][NTT][2], t2[2][NTT][2], t3[2][NTT][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < NTT; ++b)
 #pragma unroll
       for (int v = 0; v < 2; ++v) t1[a][b][v] = t2[a][b][v] = t3[a][b][v] = 0.0;
 
@@ -121,7 +126,7 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       const int ka = kk + (lane & 3);
-      double ar[2], ai[2], sa[2], xr[2], xi[2], sx[2];
+      double ar[2], ai[2], sa[2], xr[NTT], xi[NTT], sx[NTT];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int m = warp * 16 + mt * 8 + (lane >> 2);
@@ -130,7 +135,7 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
         sa[mt] = ar[mt] + ai[mt];
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int nt = 0; nt < NTT; ++nt) {
         const int n = nt * 8 + (lane >> 2);
         xr[nt] = sXr[buf][ka][n];
         xi[nt] = sXi[buf][ka][n];
@@ -140,26 +145,26 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma(t1[mt][nt][0], t1[mt][nt][1], ar[mt], xr[nt]);
+        for (int nt = 0; nt < NTT; ++nt) dmma(t1[mt][nt][0], t1[mt][nt][1], ar[mt], xr[nt]);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma(t2[mt][nt][0], t2[mt][nt][1], ai[mt], xi[nt]);
+        for (int nt = 0; nt < NTT; ++nt) dmma(t2[mt][nt][0], t2[mt][nt][1], ai[mt], xi[nt]);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma(t3[mt][nt][0], t3[mt][nt][1], sa[mt], sx[nt]);
+        for (int nt = 0; nt < NTT; ++nt) dmma(t3[mt][nt][0], t3[mt][nt][1], sa[mt], sx[nt]);
     }
     if (t + 1 < total) {
       __syncthreads();  // everyone done reading sX[buf ^ 1] of tile t - 1
       store_x(buf ^ 1, xreg);
     }
   }
-  double yr[2][2][2], yi[2][2][2];
+  double yr[2][NTT][2], yi[2][NTT][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < NTT; ++b)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         yr[a][b][v] = t1[a][b][v] - t2[a][b][v];
@@ -170,7 +175,7 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < NTT; ++nt)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
@@ -184,7 +189,7 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NTT; ++nt)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
@@ -201,6 +206,14 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
         G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
       }
 }
+
+extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
+  zgemm_taylor<2>(G);
+}
+extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor_n32(const __grid_constant__ LgGemmArgs G) {
+  zgemm_taylor<4>(G);
+}
+extern "C" int lg_zgemm_smem_bytes(int ntt) { return (int)sizeof(double) * (4 * BK * SA + 4 * BK * (8 * ntt + 1)); }
 
 // Split-k finish: y = sum of the k-slices in slice order (deterministic), then the Taylor update.
 extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G) {
@@ -320,6 +333,7 @@ extern "C" __global__ void lg_k_ell_taylor(const __grid_constant__ LgEllTaylorAr
 
 extern "C" void* lg_ell_taylor_kernel() { return (void*)lg_k_ell_taylor; }
 extern "C" void* lg_zgemm_kernel() { return (void*)lg_k_zgemm_taylor; }
+extern "C" void* lg_zgemm_n32_kernel() { return (void*)lg_k_zgemm_taylor_n32; }
 extern "C" void* lg_taylor_epi_kernel() { return (void*)lg_k_taylor_epi; }
 extern "C" void* lg_dense_form_kernel() { return (void*)lg_k_dense_form; }
 extern "C" void* lg_dots_kernel() { return (void*)lg_k_dots; }

@@ -29,8 +29,22 @@ int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2*
   // split-k when the output tiles alone cannot fill the GPU (tall-skinny Taylor terms, 4 warps per
   // 64 x 16 tile): deterministic, slices summed in order by lg_k_taylor_epi.  Measured at d = 4096:
   // C = 64: 22.6 (1 slice) -> 29.7 TF/s (4); C = 128: 25.8 -> 31.2 TF/s (4) (tools/bench_zgemm.py).
-  const long nct = (long)((C + 15) / 16) * ((d + 63) / 64);
-  int ks = (int)std::max<long>(1, std::min<long>(4, 2048L / std::max<long>(nct, 1)));
+  // wide tile (4 warps of 16 x 32) from 64 columns: half the A-fragment loads per DMMA
+  // (tools/bench_zgemm.py, d = 4096: C = 64 33.0 -> 34.3, C = 128 35.0 -> 35.9 TF/s, split-k 8)
+  const char* ev = std::getenv("LG_ZGEMM_N32");
+  const int n32_from = ev ? std::atoi(ev) : 64;
+  const int ntt = n32_from > 0 && C >= n32_from ? 4 : 2;
+  const int bn = 8 * ntt;
+  const int smem = lg_zgemm_smem_bytes(ntt);
+  void* kern = ntt == 4 ? lg_zgemm_n32_kernel() : lg_zgemm_kernel();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(lg_zgemm_n32_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, lg_zgemm_smem_bytes(4));
+    cudaFuncSetAttribute(lg_zgemm_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, lg_zgemm_smem_bytes(2));
+    attr_set = true;
+  }
+  const long nct = (long)((C + bn - 1) / bn) * ((d + 63) / 64);
+  int ks = (int)std::max<long>(1, std::min<long>(ntt == 4 ? 8 : 4, 2048L / std::max<long>(nct, 1)));
   if (const char* e = std::getenv("LG_SPLITK")) ks = std::max(1, std::atoi(e));
   G.ksplit = ks;
   if (ks > 1) {
@@ -45,7 +59,7 @@ int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2*
     G.partial = p->d_splitws;
   }
   void* args[] = {&G};
-  int rc = launch(lg_zgemm_kernel(), dim3((C + 15) / 16, (d + 63) / 64, ks), dim3(128), args, 0, p->stream);
+  int rc = launch(kern, dim3((C + bn - 1) / bn, (d + 63) / 64, ks), dim3(128), args, smem, p->stream);
   if (rc || ks == 1) return rc;
   const long mc = (long)d * C;
   return launch(lg_taylor_epi_kernel(), dim3((unsigned)std::min<long>((mc + 255) / 256, 148 * 8)), dim3(256), args, 0,
