@@ -425,6 +425,44 @@ class Step:
         return taylor_apply(mv, stacked, m, s)[:d]
 
 
+DEGENERACY_RTOL = 1e-12  # src/derivatives.py:45
+
+
+class DiagStep:
+    """DIAGONALIZATION backend step (src/derivatives.py:228-275): eigenfactorisation of the
+    dense step matrix H_n dt, exact propagators and the divided-difference derivative."""
+
+    def __init__(self, h_static, h_controls, amps_n, dt, tau):
+        self.h_controls = h_controls
+        self.dt = dt
+        h = combine([1.0] + [complex(x) for x in amps_n], [h_static, *h_controls])
+        w, self.vecs = np.linalg.eigh(to_dense(h) * dt)  # src/derivatives.py:230-231
+        self.eig = -1j * w.astype(np.complex128)
+        self.exp = np.exp(self.eig)
+        gaps = self.eig[None, :] - self.eig[:, None]
+        scale_ = float(np.abs(w).max()) if w.size else 0.0
+        degenerate = np.abs(gaps) <= DEGENERACY_RTOL * max(scale_, 1e-300)
+        inv = np.zeros_like(gaps)
+        np.divide(1.0, gaps, out=inv, where=~degenerate)
+        self.hadamard = (self.exp[None, :] - self.exp[:, None]) * inv + np.diag(self.exp)
+
+    def _prop(self, psi, adjoint):
+        c = self.vecs.conj().T @ psi
+        return self.vecs @ ((np.conj(self.exp) if adjoint else self.exp) * c)
+
+    def forward(self, psi):
+        return self._prop(psi, False)
+
+    def adjoint(self, psi):
+        return self._prop(psi, True)
+
+    def dU(self, k, psi):  # src/derivatives.py:249-275
+        da = to_dense(self.h_controls[k]) * (-1j * self.dt)
+        s = self.vecs
+        inner = s.conj().T @ da @ s
+        return s @ ((self.hadamard * inner) @ (s.conj().T @ psi))
+
+
 def plan_table(h_static, h_controls, amps, dt, tau):
     """Per-step planner inputs and plans: returns dict of arrays
     norm1[N], sp[N], m[N], s[N], aux_arg[N,Kc], aux_sp[N,Kc], aux_m, aux_s."""
@@ -473,6 +511,7 @@ class Problem:
     tau: float = 1e-8
     initial_states: np.ndarray | None = None  # (K, d) state-transfer trajectories
     basis: np.ndarray | None = None  # (K, d) gate basis (computational basis if None)
+    backend: str = "scaling_squaring"  # or "diagonalization" (src/derivatives.py:48-51)
 
 
 class _Memo:
@@ -484,7 +523,8 @@ class _Memo:
 
     def get(self, n):
         if n != self.n:
-            self.st = Step(self.p.h_static, self.p.h_controls, self.amps[n], self.dt, self.p.tau)
+            cls = DiagStep if self.p.backend == "diagonalization" else Step
+            self.st = cls(self.p.h_static, self.p.h_controls, self.amps[n], self.dt, self.p.tau)
             self.n = n
         return self.st
 

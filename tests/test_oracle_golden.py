@@ -116,6 +116,26 @@ def test_stress_cost_grad(tag):
         assert G.grad_rel(grad, z[gk]) <= 1e-12
 
 
+@pytest.mark.parametrize("tag", ["d_dense40", "d_csr24", "d_csr60"])
+def test_diagonalization_backend_cost_grad(tag):
+    """The oracle's DIAGONALIZATION restatement against the reference's own backend."""
+    z = G.sub(G.load("diag"), tag)
+    hs, hc = G.mats(z, "oracle")
+    om = G.penalty(z, "oracle")
+    p = O.Problem(hs, tuple(hc), initial_states=z["psi0"], basis=z["basis"], backend="diagonalization")
+    dt = float(z["dt"])
+    terms = [O.Term(O.STATE_INFIDELITY, 0.7, z["targets"]), O.Term(O.STATE_PENALTY, 0.2, None, om),
+             O.Term(O.STATE_RUNNING_INFIDELITY, 0.4, z["targets"])]
+    cost, grad = O.composite_grad(p, z["amps"], dt, terms)
+    assert abs(cost - float(z["cost_state"])) <= 1e-13
+    assert G.grad_rel(grad, z["grad_state"]) <= 1e-12
+    assert abs(O.composite_cost(p, z["amps"], dt, terms) - float(z["cost_state_only"])) <= 1e-13
+    for kind, ck, gk in [(O.GATE_INFIDELITY, "cost_g1", "grad_g1"), (O.GATE_RUNNING_INFIDELITY, "cost_g3", "grad_g3")]:
+        cost, grad = O.composite_grad(p, z["amps"], dt, [O.Term(kind, 1.0, z["images"])])
+        assert abs(cost - float(z[ck])) <= 1e-13
+        assert G.grad_rel(grad, z[gk]) <= 1e-12
+
+
 @pytest.mark.slow
 def test_c2_cost_grad_full_size():
     z = G.load("c2")
