@@ -149,8 +149,10 @@ def critical_path_terms(plan_table):
 
 
 def cpu_reference(case, budget_s=20.0):
-    """Time the oracle port of the reference algorithm on a bounded prefix (one process per
-    trajectory).  Returns (evals_per_s_extrapolated, cores, sample description)."""
+    """Time the oracle port of the reference algorithm on a bounded prefix, one process per
+    (trajectory, cost term): the composite is a weighted sum of per-term passes
+    (src/costs.py:515-546), so every pass of every trajectory is independent work for the
+    host cores.  Returns (evals_per_s_extrapolated, cores, sample description)."""
     import multiprocessing as mp
 
     from oracle import lg_oracle as O
@@ -158,25 +160,27 @@ def cpu_reference(case, budget_s=20.0):
     N = case.field.n_steps
     # probe one step to size the sample to ~budget_s of CPU work per trajectory
     t0 = time.perf_counter()
-    _ref_traj_worker((case.name, 0, 4))
+    _ref_traj_worker((case.name, 0, 4, None))
     per_step = (time.perf_counter() - t0) / 4
     n_pref = int(max(4, min(N, budget_s / max(per_step, 1e-6))))
     T = case.n_states
-    cores = max(1, min(T, os.cpu_count() or 1))
+    items = [(case.name, t, n_pref, ti) for t in range(T) for ti in range(len(case.terms))]
+    cores = max(1, min(len(items), len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)))
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
-        pool.map(_ref_traj_worker, [(case.name, t, n_pref) for t in range(T)])
+        pool.map(_ref_traj_worker, items, chunksize=1)
     wall = time.perf_counter() - t0
     per_eval = wall * (N / n_pref)
-    sample = (f"oracle port of the reference (oracle/lg_oracle.py), {T} trajectories x {n_pref}/{N} steps "
-              f"in {cores} processes, {wall:.1f}s wall, extrapolated linearly to N={N}")
+    sample = (f"oracle port of the reference (oracle/lg_oracle.py), {T} trajectories x {len(case.terms)} cost-term "
+              f"passes x {n_pref}/{N} steps in {cores} processes, {wall:.1f}s wall, extrapolated linearly to N={N}")
     del O
     return 1.0 / per_eval, cores, sample
 
 
 def _ref_traj_worker(arg):
-    """One trajectory's forward+backward with the oracle (the reference algorithm)."""
-    name, t, n_pref = arg
+    """One trajectory's forward+backward with the oracle (the reference algorithm), for one cost
+    term (ti) or all of them (ti None)."""
+    name, t, n_pref, ti = arg
     from oracle import lg_oracle as O
     from paper_2304_06200_b200 import models
 
@@ -200,6 +204,8 @@ def _ref_traj_worker(arg):
         else:
             tg = term.target_state if term.target_state is not None else term.target_images
             terms.append(O.Term(k, term.weight, np.asarray(tg)[t:t + 1]))
+    if ti is not None:
+        terms = [terms[ti]]
     O.composite_grad(op, case.field.amplitudes, case.field.dt, terms)
     return t
 
