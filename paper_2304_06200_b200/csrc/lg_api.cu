@@ -117,6 +117,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ++g_launches;
+    ensure_smem(f, cfg.dynamicSmemBytes);
     cudaError_t e = cudaLaunchKernelExC(&cfg, f, eargs);
     if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
     return LG_OK;
@@ -156,7 +157,9 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       ++g_launches;
-      cudaError_t e = cudaLaunchKernelExC(&cfg, lg_ws_kernel(2, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl), eargs);
+      void* wsc = lg_ws_kernel(2, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl);
+      ensure_smem(wsc, cfg.dynamicSmemBytes);
+      cudaError_t e = cudaLaunchKernelExC(&cfg, wsc, eargs);
       if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("cluster launch: ") + cudaGetErrorString(e));
     } else {
       rc = launch(bwd, grid, bblock, eargs, bsm, p->stream, p->multi);

@@ -37,12 +37,7 @@ int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2*
   const int bn = 8 * ntt;
   const int smem = lg_zgemm_smem_bytes(ntt);
   void* kern = ntt == 4 ? lg_zgemm_n32_kernel() : lg_zgemm_kernel();
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(lg_zgemm_n32_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, lg_zgemm_smem_bytes(4));
-    cudaFuncSetAttribute(lg_zgemm_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, lg_zgemm_smem_bytes(2));
-    attr_set = true;
-  }
+  // (launch() raises the kernel's dynamic shared-memory limit to `smem` when it exceeds 48 KB)
   const long nct = (long)((C + bn - 1) / bn) * ((d + 63) / 64);
   int ks = (int)std::max<long>(1, std::min<long>(ntt == 4 ? 8 : 4, 2048L / std::max<long>(nct, 1)));
   if (const char* e = std::getenv("LG_SPLITK")) ks = std::max(1, std::atoi(e));

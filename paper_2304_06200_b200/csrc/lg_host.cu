@@ -187,8 +187,16 @@ int ensure_N(lg_problem* p, long N) {
 
 long long g_launches = 0;  // kernels this library launched (lg_launch_count)
 
+// The dynamic shared-memory limit is a per-function (per-device) attribute: problems that share a
+// kernel but not its size set it before each launch, so one problem's setting never truncates
+// another's.
+void ensure_smem(void* f, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop) {
   ++g_launches;
+  ensure_smem(f, smem);
   cudaError_t e = coop ? cudaLaunchCooperativeKernel(f, grid, block, args, smem, st)
                        : cudaLaunchKernel(f, grid, block, args, smem, st);
   if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));

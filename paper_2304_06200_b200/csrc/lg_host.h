@@ -251,6 +251,7 @@ int build_problem(const lg_problem_desc* D, lg_problem* p);
 int prepare_dt(lg_problem* p, double dt);
 int ensure_N(lg_problem* p, long N);
 int launch(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st, bool coop = false);
+void ensure_smem(void* f, size_t smem);
 int prepare_steps(lg_problem* p, long N, double dt, bool need_aux);
 int prepare_diag(lg_problem* p, long N, double dt, bool need_aux);  // lg_diag.cu
 LgEngineArgs engine_args(lg_problem* p, long N);
