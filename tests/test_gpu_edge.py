@@ -188,3 +188,35 @@ def test_planning_error_and_bad_inputs():
         composite_grad(prob, ControlField(*bad.shape, c["dt"], bad), terms)
     with pytest.raises(ValueError):
         composite_grad(prob, ControlField(4, 2, c["dt"], c["amps"][:, :2]), terms)
+
+
+def test_interleaved_problems_sharing_kernels():
+    """Problems that share a kernel with different shared-memory sizes (and engines), evaluated
+    alternately: each launch must carry its own dynamic shared-memory limit."""
+    import _golden as G2
+    from paper_2304_06200_b200 import models
+
+    z3 = G2.load("c3")
+    hs, hc = G2.mats(z3)
+    p3 = ControlProblem(hs, tuple(hc), initial_state=z3["psi0"])
+    a3 = ControlField(z3["amps"].shape[0], 2, float(z3["dt"]), z3["amps"])
+    t3 = [CostTerm(CostKind.STATE_INFIDELITY, 1.0, target_state=z3["targets"])]
+    zs = G2.sub(G2.load("stress"), "s_block160")
+    hs2, hc2 = G2.mats(zs)
+    N, Kc = zs["amps"].shape
+    a2 = ControlField(N, Kc, float(zs["dt"]), zs["amps"])
+    p2 = ControlProblem(hs2, tuple(hc2), initial_state=zs["psi0"])
+    t2 = [CostTerm(CostKind.STATE_INFIDELITY, 0.7, target_state=zs["targets"]),
+          CostTerm(CostKind.STATE_PENALTY, 0.2, penalty_op=G2.penalty(zs)),
+          CostTerm(CostKind.STATE_RUNNING_INFIDELITY, 0.4, target_state=zs["targets"])]
+    c2 = models.build_case("c2", n_steps=50)
+    n3 = NativeProblem(p3, t3, initial_states=z3["psi0"])
+    n2 = NativeProblem(p2, t2, initial_states=zs["psi0"])
+    r_c2 = composite_grad(c2.problem, c2.field, c2.terms)
+    for _ in range(2):
+        r = n3.grad(a3)
+        assert abs(r.cost - float(z3["cost"])) <= 1e-12 and G2.grad_rel(r.grad, z3["grad"]) <= 1e-9
+        r = n2.grad(a2)
+        assert abs(r.cost - float(zs["cost_state"])) <= 1e-12 and G2.grad_rel(r.grad, zs["grad_state"]) <= 1e-9
+        r = composite_grad(c2.problem, c2.field, c2.terms)
+        assert r.cost == r_c2.cost and np.array_equal(r.grad, r_c2.grad)
