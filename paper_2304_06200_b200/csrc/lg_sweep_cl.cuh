@@ -211,6 +211,14 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
   // reuses another row's address), and garbage left to grow there could reach Inf (0 * Inf).
   const int pos = c.H + c.li;
   const bool keep = pos >= vt * c.H && pos < c.WIN - vt * c.H;
+  // packed slot columns: loaded once per term (a store to the window between columns would
+  // otherwise make the compiler reload them for every column)
+  unsigned cw[(W + 3) / 4];
+  {
+    const unsigned* ct = reinterpret_cast<const unsigned*>(cl_sm + c.cols) + c.li;
+#pragma unroll
+    for (int k = 0; k < (W + 3) / 4; ++k) cw[k] = ct[k * c.T];
+  }
 #pragma unroll
   for (int q = 0; q < MAXC; ++q) {
     if (q >= C) break;
@@ -218,10 +226,6 @@ __device__ __forceinline__ void term_row(const LgEngineArgs& E, const Cl& c, ClR
     if (c.ex && (c.slot || !fin)) {
       const int xc = X + q * c.WIN + c.H + c.li;
       double2 p1 = make_double2(0.0, 0.0), pq1 = make_double2(0.0, 0.0);
-      const unsigned* ct = reinterpret_cast<const unsigned*>(cl_sm + c.cols) + c.li;
-      unsigned cw[(W + 3) / 4];
-#pragma unroll
-      for (int k = 0; k < (W + 3) / 4; ++k) cw[k] = ct[k * c.T];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const double2 x = cl_sm[slot_col(cw[w >> 2], w, xc)];
