@@ -104,10 +104,15 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   }
   auto cl_launch = [&](void* f, bool backward) -> int {
     E.cl_acs = backward ? p->cl_acs : 0;
+    const bool split = backward && p->cl_split;
+    E.cl_R = split ? p->cl_R_b : p->cl_R;
+    E.cl_Q = split ? p->cl_Q_b : p->cl_Q;
+    E.cl_E = split ? p->cl_E_b : p->cl_E;
+    if (split) f = lg_cl_kernel(1, p->W, p->cl_maxc, 2);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p->n_groups * p->cl_CS);
-    cfg.blockDim = dim3(p->threads);
-    cfg.dynamicSmemBytes = backward ? p->cl_smem_b : p->cl_smem;
+    cfg.blockDim = dim3(split ? p->cl_T_b : p->threads);
+    cfg.dynamicSmemBytes = split ? p->cl_smem_split : (backward ? p->cl_smem_b : p->cl_smem);
     cfg.stream = p->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -358,7 +363,7 @@ const char* lg_engine_name(lg_problem* p) {
     case 2: return "cta:lg_k_cta_backward";
     case 3: return "dense:lg_k_zgemm_taylor";
     case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
-    case 5: return "cluster:lg_k_cl_backward";
+    case 5: return p->cl_split ? "cluster-split:lg_k_cl_backward" : "cluster:lg_k_cl_backward";
     default: return "unknown";
   }
 }

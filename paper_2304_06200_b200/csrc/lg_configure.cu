@@ -296,6 +296,48 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_acs = acs ? 1 : 0;
   p->cta_Imax = Imax;
   p->threads = 32 * ((R + 2 * E + 31) / 32);
+  // Split backward (lg_k_cl_backward<..., SPLIT>): the cluster's two halves run the adjoint
+  // chain and the aux chains of consecutive steps concurrently over a row partition of
+  // R_b = d / (CS / 2) rows.  Taken when the SMALL kernel fits (<= 192 threads, two CTAs per
+  // SM) and every trajectory's cluster stays resident.
+  p->cl_split = 0;
+  if (small && CS == 16 && p->Kc >= 1 && !(std::getenv("LG_CL_SPLIT") && std::atoi(std::getenv("LG_CL_SPLIT")) == 0)) {
+    const int rb = (int)((d + 7) / 8);
+    int qb = rb <= 200 ? std::max(1, std::min(6, 1 + ((H + 7) / 8 * 8) / H)) : 1;
+    while (qb > 1 && (ext(qb) + H > rb)) --qb;
+    const int eb = ext(qb), tb = 32 * ((rb + 2 * eb + 31) / 32);
+    const int acw = acs ? p->Kc * p->Wc : 0;
+    const int ws = lg_cl_smem_words(rb, H, qb, eb, cmax, p->W, acw) + 3 + 2 * cst * rb;  // + mbarriers, hand-off ring
+    void* fs = lg_cl_kernel(1, p->W, maxc, 2);
+    if (rb >= eb + H && tb <= 192 && fs && (long)ws * 16 <= cap &&
+        cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, ws * 16) == cudaSuccess &&
+        cudaFuncSetAttribute(fs, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(tb);
+      cfg.dynamicSmemBytes = ws * 16;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, fs, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        ncl = 0;
+      }
+      if (ncl >= (int)gset.size()) {
+        p->cl_split = 1;
+        p->cl_R_b = rb;
+        p->cl_Q_b = qb;
+        p->cl_E_b = eb;
+        p->cl_T_b = tb;
+        p->cl_smem_split = ws * 16;
+      }
+    }
+  }
   p->n_slabs = 1;
   p->grp_set = gset;
   p->grp_t0 = gt0;

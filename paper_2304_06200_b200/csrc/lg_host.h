@@ -150,6 +150,7 @@ struct lg_problem {
   double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
   size_t splitws_cap = 0;
   // cluster engine
+  int cl_split = 0, cl_R_b = 0, cl_Q_b = 1, cl_E_b = 0, cl_T_b = 0, cl_smem_split = 0;  // split backward
   int cl_CS = 0, cl_R = 0, cl_H = 0, cl_Q = 1, cl_E = 0, cl_small = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
   unsigned char* d_cl_slot = nullptr;

@@ -111,9 +111,16 @@ struct Cl {
   int Cmax, Cst, Wc;
   int acs, accs;                        // staged control rows: double2 [Kc][Wc][T] and int [Kc][Wc][T] (-1: not staged)
   int cols;                             // packed slot columns, unsigned [(W+3)/4][T]
-  int mb;                               // two mbarriers (exchange buffers tb0 / tb1), 8-byte words after the layout
+  int mb;                               // mbarriers (8-byte words after the layout): [0,1] exchange buffers tb0 / tb1,
+                                        // split backward: [2] group barrier, [3, 3+HR) hand-off full, [3+HR, 3+2HR) empty
   mutable unsigned ph;                  // parity bits of the next phase of mb[0], mb[1]
+  // split backward (adjoint / aux CTA groups of one cluster; otherwise the group is the cluster)
+  bool split;
+  int group, base;                      // group index, cluster rank of the group's rank 0 (c.rank, c.CS are group-local)
+  mutable unsigned gph;                 // parity of the group barrier's next phase
+  int hring;                            // hand-off ring [HR][Cst][R] (double2), after the mbarriers
 };
+constexpr int LG_CL_HR = 2;  // hand-off ring depth (split backward)
 
 // SMALL: the CTA has <= 256 threads (few rows per CTA, latency-bound), so the
 // full register file is available: gather offsets live in registers and every
@@ -136,8 +143,8 @@ __device__ __forceinline__ int slot_col(unsigned word, int w, int base) {
 __device__ __forceinline__ void put(const Cl& c, int buf, int colo, double2 v) {
   const int off = buf + colo * c.WIN, oi = c.li - c.E;
   cl_sm[off + c.H + c.li] = v;
-  if (oi < c.HW && c.rank > 0) cl_st(cl_map(&cl_sm[off + c.R + c.HW + oi], c.rank - 1), v);
-  if (oi >= c.R - c.HW && c.rank + 1 < c.CS) cl_st(cl_map(&cl_sm[off + oi - c.R + c.HW], c.rank + 1), v);
+  if (oi < c.HW && c.rank > 0) cl_st(cl_map(&cl_sm[off + c.R + c.HW + oi], c.base + c.rank - 1), v);
+  if (oi >= c.R - c.HW && c.rank + 1 < c.CS) cl_st(cl_map(&cl_sm[off + oi - c.R + c.HW], c.base + c.rank + 1), v);
 }
 __device__ __forceinline__ unsigned long long* cl_mb(const Cl& c, int k) {
   return reinterpret_cast<unsigned long long*>(cl_sm + c.mb) + k;
@@ -149,9 +156,9 @@ __device__ __forceinline__ void put_async(const Cl& c, int buf, int yi, int colo
   cl_sm[off + c.H + c.li] = v;
   const unsigned mb = smaddr(cl_mb(c, yi));
   if (oi < c.HW && c.rank > 0)
-    cl_st_async(cl_map(&cl_sm[off + c.R + c.HW + oi], c.rank - 1), v, cl_map_u(mb, c.rank - 1));
+    cl_st_async(cl_map(&cl_sm[off + c.R + c.HW + oi], c.base + c.rank - 1), v, cl_map_u(mb, c.base + c.rank - 1));
   if (oi >= c.R - c.HW && c.rank + 1 < c.CS)
-    cl_st_async(cl_map(&cl_sm[off + oi - c.R + c.HW], c.rank + 1), v, cl_map_u(mb, c.rank + 1));
+    cl_st_async(cl_map(&cl_sm[off + oi - c.R + c.HW], c.base + c.rank + 1), v, cl_map_u(mb, c.base + c.rank + 1));
 }
 // Block exchange over the neighbour-only mbarriers (replaces one cluster barrier per
 // block).  Buffer yi's mbarrier is armed (one arrival + the expected halo bytes) when
@@ -163,6 +170,27 @@ __device__ __forceinline__ void put_async(const Cl& c, int buf, int yi, int colo
 __device__ __forceinline__ void exchange_begin(const Cl& c, int yi, int C) {
   if (threadIdx.x == 0)
     mb_arm(cl_mb(c, yi), 16u * (unsigned)(c.HW * C) * ((c.rank > 0 ? 1u : 0u) + (c.rank + 1 < c.CS ? 1u : 0u)));
+}
+// Barrier over the CTA's group: the cluster barrier when the group is the whole cluster; in the
+// split backward every CTA's threads 0..CS-1 release-arrive on the group members' barrier
+// mbarriers (count CS) after a CTA barrier, and the CTA waits on its own (acquire, cluster scope).
+__device__ __forceinline__ void gsync(const Cl& c) {
+  if (!c.split) {
+    cl_sync();
+    return;
+  }
+  __syncthreads();
+  unsigned long long* gb = cl_mb(c, 2);
+  if ((int)threadIdx.x < c.CS)
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                     cl_map_u(smaddr(gb), c.base + threadIdx.x))
+                 : "memory");
+  asm volatile(
+      "{\n .reg .pred p;\n GW_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra GW_%=;\n}\n" ::"r"(
+          smaddr(gb)),
+      "r"(c.gph & 1u)
+      : "memory");
+  c.gph ^= 1u;
 }
 __device__ __forceinline__ void exchange_end(const Cl& c, int yi) {
   __syncthreads();
@@ -185,15 +213,15 @@ __device__ void cl_reduce(const Cl& c, double2 (&v)[NV], int nv) {
     const int q = threadIdx.x;
     double2 s = make_double2(0.0, 0.0);
     for (int k = 0; k < nw; ++k) s = cadd(s, scr[q * 32 + k]);
-    for (int r = 0; r < c.CS; ++r) cl_st(cl_map(&box[q * c.CS + c.rank], r), s);
+    for (int r = 0; r < c.CS; ++r) cl_st(cl_map(&box[q * c.CS + c.rank], c.base + r), s);
   }
-  cl_sync();
+  gsync(c);
   for (int q = 0; q < nv; ++q) {
     double2 s = make_double2(0.0, 0.0);
     for (int r = 0; r < c.CS; ++r) s = cadd(s, box[q * c.CS + r]);
     v[q] = s;
   }
-  cl_sync();  // box may be rewritten by the next reduction
+  gsync(c);  // box may be rewritten by the next reduction
 }
 
 // One Taylor chain over C columns of the window buffers, input staged in tb0
@@ -344,7 +372,7 @@ template <int W, int MAXC, bool SMALL>
 __device__ __forceinline__ void chain(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, SMALL>& R, int C, int mode, int G,
                                       int m, int s, double sgn) {
   if (threadIdx.x < m) cl_sm[c.rt + threadIdx.x].x = sgn * (1.0 / (double)(s * (threadIdx.x + 1)));
-  cl_sync();  // staged input (incl. pushed halos) and the 1/(s j) table published
+  gsync(c);  // staged input (incl. pushed halos) and the 1/(s j) table published
   if constexpr (SMALL) {
 #define LG_NC(n)                                                            \
   if constexpr (n <= MAXC)                                                  \
@@ -378,7 +406,7 @@ __device__ __forceinline__ void chain(const LgEngineArgs& E, const Cl& c, ClRegs
       yi ^= 1;
     }
   }
-  cl_sync();  // every CTA done reading its windows: the caller may stage the next chain's input
+  gsync(c);  // every CTA done reading its windows: the caller may stage the next chain's input
 }
 
 template <int W, int MAXC, bool SMALL>
@@ -403,11 +431,21 @@ __device__ __forceinline__ void load_cols(const LgEngineArgs& E, const Cl& c, Cl
   }
 }
 
-__device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst, int W) {
+__device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst, int W, bool split = false) {
   Cl c;
   c.d = E.d;
+  c.split = split;
   c.CS = (int)cl_size();
   c.rank = (int)cl_rank();
+  c.group = 0;
+  c.base = 0;
+  c.gph = 0;
+  if (split) {  // two groups of CS / 2 CTAs over the same row partition
+    c.CS /= 2;
+    c.group = c.rank / c.CS;
+    c.base = c.group * c.CS;
+    c.rank -= c.base;
+  }
   c.R = E.cl_R;
   c.H = E.cl_H;
   c.Q = E.cl_Q;
@@ -454,6 +492,7 @@ __device__ __forceinline__ Cl make_cl(const LgEngineArgs& E, int Cmax, int Cst, 
   c.st = c.nx = 0;
   c.mb = lg_cl_mb_word(c.R, c.H, c.Q, c.E, Cmax, W, E.cl_acs ? E.Kc * E.Wc : 0);
   c.ph = 0;
+  c.hring = c.mb + 4;  // after 8 mbarrier words (exchange 2, group 1, hand-off 2 x HR)
   return c;
 }
 
@@ -558,13 +597,19 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __
 }
 
 // ------------------------------------------------------------------------------------------ backward
-template <int W, int MAXC, bool SMALL>
-__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const __grid_constant__ LgEngineArgs E) {
+// SPLIT (SMALL only): the cluster's CTAs form two groups over the same row partition -- group 0
+// runs the adjoint chain and the costates, group 1 the aux (derivative) chains and the inner
+// products of step n while group 0 already works on step n - 1.  psi_{n-1} and lambda_s(n) go
+// from each group-0 CTA to its group-1 partner through a hand-off ring (st.async + mbarriers).
+template <int W, int MAXC, bool SMALL, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 : 1)
+    lg_k_cl_backward(const __grid_constant__ LgEngineArgs E) {
   const int g = blockIdx.x / (int)cl_size();
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
   const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
-  Cl c = make_cl(E, cmax, cst, W);
+  Cl c = make_cl(E, cmax, cst, W, SPLIT);
+  const bool doA = !SPLIT || c.group == 0, doB = !SPLIT || c.group == 1;
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
   // zero everything up to the end of the window buffers (pad gathers may read a few rows past a
@@ -574,6 +619,10 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
   if (threadIdx.x == 0) {
     mb_init(cl_mb(c, 0), 1);
     mb_init(cl_mb(c, 1), 1);
+    if (SPLIT) {
+      mb_init(cl_mb(c, 2), c.CS);
+      for (int h = 0; h < 2 * LG_CL_HR; ++h) mb_init(cl_mb(c, 3 + h), 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (c.acs >= 0)
@@ -586,8 +635,9 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
   // state: psi (column 0) and the costates lambda_s (columns 1 + s), own rows in registers
   double2 psi = c.own ? E.psiN[(long)t0 * c.d + c.orig] : make_double2(0.0, 0.0);
   double2 lam[LG_MAX_SPECS];
+  for (int si = 0; si < LG_MAX_SPECS; ++si) lam[si] = make_double2(0.0, 0.0);
   // ---- costate initialisation (src/costs.py:312-321, :457-460)
-  {
+  if (doA) {
     bool anypen = false, anyrun = false;
     for (int si = 0; si < I; ++si) {
       const int k = E.spec[E.set_spec[set][si]].kind;
@@ -596,7 +646,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
     }
     if (anypen) {
       if (c.slot) put(c, c.tb0, 0, psi);
-      cl_sync();
+      gsync(c);
     }
     double2 ov[LG_MAX_SPECS];
     for (int si = 0; si < LG_MAX_SPECS; ++si) ov[si] = make_double2(0.0, 0.0);
@@ -627,27 +677,58 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
       }
       lam[si] = v;
     }
-    cl_sync();
+    gsync(c);
   }
   int gch[LG_MAX_CHANNELS];
-  for (int n = N - 1; n >= 0; --n) {
+  for (int n = N - 1, it = 0; n >= 0; --n, ++it) {
     const int4* pln = E.plan + (long)n * (Kc + 1);
     const int4 pl = pln[0];
     load_row<W, MAXC, SMALL>(E, c, n, R);
-    // adjoint chain on [psi | lambda] (src/costs.py:326,342); costates not needed at n == 0
-    const int cadj = n > 0 ? 1 + I : 1;
-    if (c.slot) {
-      put(c, c.tb0, 0, psi);
-      for (int si = 0; si < I && n > 0; ++si) put(c, c.tb0, 1 + si, lam[si]);
+    double2 psip = make_double2(0.0, 0.0);  // psi_{n-1}
+    double2 lamn[LG_MAX_SPECS];             // U_n^dagger lambda_s(n)
+    double2 lamc[LG_MAX_SPECS];             // lambda_s(n) for the inner products
+    for (int si = 0; si < LG_MAX_SPECS; ++si) lamn[si] = lamc[si] = lam[si];
+    const int hs = it % LG_CL_HR;
+    if (doA) {
+      // adjoint chain on [psi | lambda] (src/costs.py:326,342); costates not needed at n == 0
+      const int cadj = n > 0 ? 1 + I : 1;
+      if (c.slot) {
+        put(c, c.tb0, 0, psi);
+        for (int si = 0; si < I && n > 0; ++si) put(c, c.tb0, 1 + si, lam[si]);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) R.cur[q] = q == 0 ? psi : (q - 1 < I ? lam[q - 1] : make_double2(0.0, 0.0));
+      chain<W, MAXC, SMALL>(E, c, R, cadj, 0, 0, pl.x, pl.y, -1.0);
+      psip = R.cur[0];
+#pragma unroll
+      for (int q = 1; q < MAXC; ++q)
+        if (q - 1 < LG_MAX_SPECS) lamn[q - 1] = R.cur[q];
+      if (SPLIT) {  // hand psi_{n-1} and lambda_s(n) to the partner CTA of group 1
+        if (it >= LG_CL_HR) mb_wait(cl_mb(c, 3 + LG_CL_HR + hs), (unsigned)((it / LG_CL_HR) - 1) & 1u);
+        if (c.slot) {
+          const int oi = c.li - c.E, partner = c.CS + c.rank;
+          const unsigned fb = cl_map_u(smaddr(cl_mb(c, 3 + hs)), partner);
+          cl_st_async(cl_map(&cl_sm[c.hring + (hs * cst + 0) * c.R + oi], partner), psip, fb);
+          for (int si = 0; si < I; ++si)
+            cl_st_async(cl_map(&cl_sm[c.hring + (hs * cst + 1 + si) * c.R + oi], partner), lam[si], fb);
+        }
+      }
     }
-#pragma unroll
-    for (int q = 0; q < MAXC; ++q) R.cur[q] = q == 0 ? psi : (q - 1 < I ? lam[q - 1] : make_double2(0.0, 0.0));
-    chain<W, MAXC, SMALL>(E, c, R, cadj, 0, 0, pl.x, pl.y, -1.0);
-    const double2 psip = R.cur[0];  // psi_{n-1}
-    double2 lamn[LG_MAX_SPECS];     // U_n^dagger lambda_s(n)
-#pragma unroll
-    for (int q = 1; q < MAXC; ++q)
-      if (q - 1 < LG_MAX_SPECS) lamn[q - 1] = R.cur[q];
+    if (doB) {
+      if (SPLIT) {  // take psi_{n-1} and lambda_s(n) from the partner, then free the slot
+        if (threadIdx.x == 0) mb_arm(cl_mb(c, 3 + hs), 16u * (unsigned)(c.R * (1 + I)));
+        mb_wait(cl_mb(c, 3 + hs), (unsigned)(it / LG_CL_HR) & 1u);
+        if (c.slot) {
+          const int oi = c.li - c.E;
+          psip = cl_sm[c.hring + (hs * cst + 0) * c.R + oi];
+          for (int si = 0; si < I; ++si) lamc[si] = cl_sm[c.hring + (hs * cst + 1 + si) * c.R + oi];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                           cl_map_u(smaddr(cl_mb(c, 3 + LG_CL_HR + hs)), c.rank))
+                       : "memory");
+      }
     // derivative products per channel group (src/costs.py:328-339)
     unsigned done = 0;
     for (int kc = 0; kc < Kc; ++kc) {
@@ -682,7 +763,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
 #pragma unroll
             for (int q = 0; q < MAXC; ++q)
               if (q == gi) dd = R.cur[q];
-            v[gi * I + si] = cdot(lam[si], dd);
+            v[gi * I + si] = cdot(lamc[si], dd);
           }
       cl_reduce<16>(c, v, nv);
       if (c.rank == 0 && threadIdx.x == 0)
@@ -692,7 +773,12 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
             E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + t0] = v[gi * I + si];
           }
     }
+    }  // doB
     if (n == 0) break;
+    if (!doA) {
+      gsync(c);
+      continue;
+    }
     // costate sources at psi_{n-1} (src/costs.py:341-353, :474-479)
     bool anypen = false, anyrun = false;
     for (int si = 0; si < I; ++si) {
@@ -702,7 +788,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
     }
     if (anypen) {
       if (c.slot) put(c, c.tb0, 0, psip);
-      cl_sync();
+      gsync(c);
     }
     double2 ov[LG_MAX_SPECS];
     for (int si = 0; si < LG_MAX_SPECS; ++si) ov[si] = make_double2(0.0, 0.0);
@@ -729,7 +815,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
       lam[si] = v;
     }
     psi = psip;
-    cl_sync();
+    gsync(c);
   }
   cl_sync();
 }
@@ -748,4 +834,5 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_backward(const _
   case C_ * 2:                                                                                               \
     return backward ? (void*)lg_k_cl_backward<W_, C_, false> : (void*)lg_k_cl_forward<W_, C_, false>;        \
   case C_ * 2 + 1:                                                                                           \
+    if (small == 2) return backward ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;                 \
     return backward ? (void*)lg_k_cl_backward<W_, C_, true> : (void*)lg_k_cl_forward<W_, C_, true>;
