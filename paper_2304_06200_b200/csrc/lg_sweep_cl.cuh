@@ -81,6 +81,14 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
       "r"(parity)
       : "memory");
 }
+// Wait for a phase completed by another CTA's release-arrive (acquire at cluster scope).
+__device__ __forceinline__ void mb_wait_cluster(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra WC_%=;\n}\n" ::"r"(
+          smaddr(b)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
@@ -704,7 +712,7 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
       for (int q = 1; q < MAXC; ++q)
         if (q - 1 < LG_MAX_SPECS) lamn[q - 1] = R.cur[q];
       if (SPLIT) {  // hand psi_{n-1} and lambda_s(n) to the partner CTA of group 1
-        if (it >= LG_CL_HR) mb_wait(cl_mb(c, 3 + LG_CL_HR + hs), (unsigned)((it / LG_CL_HR) - 1) & 1u);
+        if (it >= LG_CL_HR) mb_wait_cluster(cl_mb(c, 3 + LG_CL_HR + hs), (unsigned)((it / LG_CL_HR) - 1) & 1u);
         if (c.slot) {
           const int oi = c.li - c.E, partner = c.CS + c.rank;
           const unsigned fb = cl_map_u(smaddr(cl_mb(c, 3 + hs)), partner);
