@@ -162,6 +162,7 @@ int ensure_N(lg_problem* p, long N) {
   p->d_parg = m.alloc<double>((size_t)N * (Kc + 1));
   p->d_psp = m.alloc<long long>((size_t)N * (Kc + 1));
   p->d_plan = m.alloc<int4>((size_t)N * (Kc + 1));
+  p->d_rtab = m.alloc<double>((size_t)N * 64);
   p->d_flag = m.alloc<int>(1);
   {
     // [ip | fin | trp | run], the lg_raw_get layout, so one all-reduce covers a shard's scalars
@@ -290,6 +291,11 @@ int prepare_steps(lg_problem* p, long N, double dt, bool need_aux) {
     }
     if (changed) CK(cudaMemcpy(p->d_plan, plans.data(), sizeof(int4) * count, cudaMemcpyHostToDevice));
   }
+  if (p->engine == 4 && !p->dense) {  // the ws chains read their per-step Taylor coefficients from this table
+    void* rargs[] = {&p->d_plan, &Kc, &Ni, &p->d_rtab};
+    rc = launch(lg_rtab_kernel(), dim3((unsigned)N), dim3(64), rargs, 0, p->stream);
+    if (rc) return rc;
+  }
   return LG_OK;
 }
 
@@ -329,6 +335,7 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.Ac_cols = p->d_ccols;
   E.Ac = p->d_Ac;
   E.plan = p->d_plan;
+  E.rtab = p->d_rtab;
   E.psi0 = p->d_traj;
   E.scratch = p->d_scratch;
   E.scratch_per_group = p->scratch_per_group;

@@ -37,6 +37,7 @@ extern "C" void* lg_taylor_epi_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc, int small);
 extern "C" int lg_cl_smem_words(int R, int H, int Q, int E, int cmax, int W, int acw);
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl);
+extern "C" void* lg_rtab_kernel();
 extern "C" int lg_ws_dense_width(int d);
 extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_bars, int dense);
 extern "C" void* lg_dense_form_kernel();
@@ -187,6 +188,7 @@ struct lg_problem {
   double *d_norm1 = nullptr, *d_aux_arg = nullptr, *d_parg = nullptr;
   long long *d_sp = nullptr, *d_aux_sp = nullptr, *d_psp = nullptr;
   int4* d_plan = nullptr;
+  double* d_rtab = nullptr;  // [N][64] Taylor coefficient table (ws engine)
   int* d_flag = nullptr;
   double2 *d_ip = nullptr, *d_fin = nullptr, *d_trp = nullptr, *d_trsum = nullptr, *d_psiN = nullptr;
   // sharded evaluation: raw scalars [ip | fin | trp | run] in one (optionally caller-lent) buffer and

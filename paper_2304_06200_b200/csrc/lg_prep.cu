@@ -313,4 +313,14 @@ extern "C" __global__ void lg_k_gather_plan_inputs(const double* norm1, const lo
 extern "C" void* lg_prep_sparse_kernel() { return (void*)lg_k_prep_sparse; }
 extern "C" void* lg_prep_dense_kernel() { return (void*)lg_k_prep_dense; }
 extern "C" void* lg_plans_kernel() { return (void*)lg_k_plans; }
+
+// Per-step Taylor coefficients 1 / (s (j + 1)) of the propagation plans, one row of 64 per step
+// (order <= 60), the same IEEE division the chains performed at the start of every step.
+extern "C" __global__ void lg_k_rtab(const int4* plan, int Kc, int N, double* rtab) {
+  const int n = blockIdx.x, j = threadIdx.x;
+  if (n >= N) return;
+  const int4 pl = plan[(long)n * (Kc + 1)];
+  rtab[(long)n * 64 + j] = j < pl.x ? 1.0 / (double)(pl.y * (j + 1)) : 0.0;
+}
+extern "C" void* lg_rtab_kernel() { return (void*)lg_k_rtab; }
 extern "C" void* lg_gather_kernel() { return (void*)lg_k_gather_plan_inputs; }

@@ -147,9 +147,11 @@ template <int W, int RPL, int NC>
 __device__ __forceinline__ void team_chain(const Team& tm, double2 (&cur)[NC][RPL], const double2 (&a)[RPL][W],
                                            const int (&col)[RPL][W], const double2 (&ac)[RPL][2],
                                            const int (&accol)[RPL][2], int m, int s, double sgn, int tb0, int tb1,
-                                           int rt) {
-  if (tm.tl < m) ws_sm[rt + tm.tl].x = sgn * (1.0 / (double)(s * (tm.tl + 1)));
-  tsync(tm);
+                                           int rt, bool build = true) {
+  if (build) {  // else the caller staged sgn / (s j) at rt from E.rtab before its last team barrier
+    if (tm.tl < m) ws_sm[rt + tm.tl].x = sgn * (1.0 / (double)(s * (tm.tl + 1)));
+    tsync(tm);
+  }
   const int total = m * s;
   int j = 1;  // position within the current scaling round
   for (int t = 0; t < total; t += 2) {
@@ -362,6 +364,13 @@ __device__ __forceinline__ void load_rows(const LgEngineArgs& E, int n, int tl, 
   }
 }
 
+template <int W>
+__device__ __forceinline__ void load_vals(const LgEngineArgs& E, int n, int i, double2 (&a)[1][W]) {
+  const double2* src = E.A + (long)n * W * E.d;
+#pragma unroll
+  for (int w = 0; w < W; ++w) a[0][w] = i < E.d ? src[(long)w * E.d + i] : make_double2(0.0, 0.0);
+}
+
 // Team-wide deterministic sum of nv (<= NV) complex values -> v[0..nv) for all team threads.
 template <int NV>
 __device__ __forceinline__ void team_reduce(const Team& tm, double2 (&v)[NV], int nv, int red) {
@@ -492,10 +501,17 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
     const double2 ac[1][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
     const int accol[1][2] = {{0, 0}};
     if (i < d) ws_sm[tb0 + i] = E.psi0[(long)t0 * d + i];
-    if (DNS)
+    const int rt = L.rt + team * 64;
+    double rnx = 0.0;  // Taylor coefficients of the next step, staged before the end-of-step barrier
+    if (DNS) {
       stage_block(E.A, L.aop, dd, tm.tl, 64);
-    else
+    } else {
       load_rows<W, 1>(E, 0, tm.tl, 64, an, coln);
+#pragma unroll
+      for (int w = 0; w < W; ++w) col[0][w] = coln[0][w];  // one ELL pattern for every step
+      ws_sm[rt + tm.tl].x = E.rtab[tm.tl];
+      team_sync(tm.id);
+    }
     int4 pln = E.plan[0];
     for (int n = 0; n < N; ++n) {
       const int4 pl = pln;
@@ -505,21 +521,25 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
         if (n + 1 < N) stage_block(E.A + (long)(n + 1) * dd, L.aop + ((n + 1) & 1) * dd, dd, tm.tl, 64);
       } else {
 #pragma unroll
-        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-        if (n + 1 < N) load_rows<W, 1>(E, n + 1, tm.tl, 64, an, coln);
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w];
+        if (n + 1 < N) {
+          load_vals<W>(E, n + 1, i, an);
+          rnx = E.rtab[(long)(n + 1) * 64 + tm.tl];
+        }
       }
       if (n + 1 < N) pln = E.plan[(long)(n + 1) * (E.Kc + 1)];
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
       if (DNS)
-        team_chain_dense_w<W>(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+        team_chain_dense_w<W>(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, rt);
       else
-        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, L.rt + team * 64);
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, rt, false);
       const int slot = n % RING, use = n / RING;
       if (use > 0) mb_wait(&empty[slot], (use - 1) & 1);
       if (i < d) {
         ws_sm[L.ring + slot * d + i] = cur[0][0];
         ws_sm[tb0 + i] = cur[0][0];
       }
+      if (!DNS) ws_sm[rt + tm.tl].x = rnx;  // the chain's last read of the table was before its last barrier
       mb_arrive(&full[slot]);
       team_sync(tm.id);
     }
@@ -1007,10 +1027,15 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
       if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN) lpsi |= 1u << si;
     }
     if (i < d) ws_sm[tb0 + i] = E.psiN[(long)t0 * d + i];
-    if (DNS)
+    double rnx = 0.0;  // Taylor coefficients of the next step, staged before the end-of-step barrier
+    if (DNS) {
       stage_block(E.A + (long)(N - 1) * dd, L.aop, dd, tl, 64);
-    else
+    } else {
       load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+#pragma unroll
+      for (int w = 0; w < W; ++w) col[0][w] = coln[0][w];  // one ELL pattern for every step
+      ws_sm[rt + tl].x = -E.rtab[(long)(N - 1) * 64 + tl];
+    }
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     team_sync(tm.id);
     for (int it = 0; it < N; ++it) {
@@ -1022,8 +1047,11 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
         if (n > 0) stage_block(E.A + (long)(n - 1) * dd, L.aop + ((it + 1) & 1) * dd, dd, tl, 64);
       } else {
 #pragma unroll
-        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-        if (n > 0) load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w];
+        if (n > 0) {
+          load_vals<W>(E, n - 1, i, an);
+          rnx = E.rtab[(long)(n - 1) * 64 + tl];
+        }
       }
       if (n > 0) pln = E.plan[(long)(n - 1) * (Kc + 1)];
       cur[0][0] = i < d ? ws_sm[tb0 + i] : make_double2(0.0, 0.0);
@@ -1032,7 +1060,7 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
       if (DNS)
         team_chain_dense_w<W>(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
       else
-        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt, false);
       if (trc && tl == 0) trc[1] = clock64();
       const int w0 = it % NW, u = it / NW, wslot = u % WR;
       for (int k = 0; k < Kc; ++k)  // the workers' slots are free (they took psi of step it - WR * NW)
@@ -1050,6 +1078,7 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
           if (lpsi & (1u << si))
             cl_st_async(cl_map(&ws_sm[L.ring + slot * d + i], 1 + si), cur[0][0], cl_map(&pfull[slot], 1 + si));
       }
+      if (!DNS) ws_sm[rt + tl].x = -rnx;  // the chain's last read of the table was before its last barrier
       team_sync(tm.id);
     }
   } else if (rank >= 1 && rank < (unsigned)(1 + I) && threadIdx.x < 64) {
@@ -1089,10 +1118,15 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
       cur[0][0] = v;
     }
     team_sync(tm.id);
-    if (DNS)
+    double rnx = 0.0;  // Taylor coefficients of this iteration's chain, loaded an iteration ahead
+    if (DNS) {
       stage_block(E.A + (long)(N - 1) * dd, L.aop, dd, tl, 64);
-    else
+    } else {
       load_rows<W, 1>(E, N - 1, tl, 64, an, coln);
+#pragma unroll
+      for (int w = 0; w < W; ++w) col[0][w] = coln[0][w];  // one ELL pattern for every step
+      rnx = E.rtab[(long)(N - 1) * 64 + tl];
+    }
     int4 pln = E.plan[(long)(N - 1) * (Kc + 1)];
     for (int it = 0; it < N; ++it) {
       const int n = N - 1 - it;
@@ -1119,8 +1153,10 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
         stage_block(E.A + (long)(n - 1) * dd, L.aop + ((it + 1) & 1) * dd, dd, tl, 64);
       } else {
 #pragma unroll
-        for (int w = 0; w < W; ++w) a[0][w] = an[0][w], col[0][w] = coln[0][w];
-        load_rows<W, 1>(E, n - 1, tl, 64, an, coln);
+        for (int w = 0; w < W; ++w) a[0][w] = an[0][w];
+        load_vals<W>(E, n - 1, i, an);
+        ws_sm[rt + tl].x = -rnx;  // the previous chain's last read of the table was before its last barrier
+        rnx = E.rtab[(long)(n - 1) * 64 + tl];
       }
       pln = E.plan[(long)(n - 1) * (Kc + 1)];
       const double2 tr = kind == LGK_GATE_RUN ? E.trsum[(long)sidx * N + n - 1] : make_double2(0.0, 0.0);
@@ -1128,7 +1164,7 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
       if (DNS)
         team_chain_dense_w<W>(tm, cur[0][0], L.aop + (it & 1) * dd, pl.x, pl.y, -1.0, tb0, tb1, rt);
       else
-        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt);
+        team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt, false);
       if (trc && tl == 0) trc[2] = clock64();
       if (needs_psi) {  // source at psi_{n-1} (src/costs.py:341-353), formed by the source warp
         mb_wait(&sfull[slot], use & 1);

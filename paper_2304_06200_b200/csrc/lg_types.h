@@ -83,6 +83,7 @@ struct LgEngineArgs {
   const int* Ac_cols;       // [Kc][Wc][d]
   const double2* Ac;        // [Kc][Wc][d]
   const int4* plan;         // [N][1+Kc] (order, scaling, status, -)
+  const double* rtab;       // [N][64] 1/(s (j+1)), j < order, of the propagation plans (ws engine, sparse)
   const double2* psi0;      // [T_total][d] initial trajectories
   // scratch
   double2* scratch;         // per group: scratch_per_group d-vectors
