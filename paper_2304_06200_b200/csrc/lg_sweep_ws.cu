@@ -61,6 +61,16 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
       "r"(parity)
       : "memory");
 }
+// Two phase waits with their SYNCS round trips overlapped (both try_waits issued before either is
+// checked; a completed phase keeps testing true until the barrier is re-armed by this thread's writes).
+__device__ __forceinline__ void mb_wait2(unsigned long long* b0, unsigned p0, unsigned long long* b1, unsigned p1) {
+  asm volatile(
+      "{\n .reg .pred p, q;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 q, [%2], %3;\n and.pred p, p, q;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smaddr(b0)),
+      "r"(p0), "r"(smaddr(b1)), "r"(p1)
+      : "memory");
+}
 // ---- cluster (DSMEM) helpers
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -1063,8 +1073,13 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
         team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, -1.0, tb0, tb1, rt, false);
       if (trc && tl == 0) trc[1] = clock64();
       const int w0 = it % NW, u = it / NW, wslot = u % WR;
-      for (int k = 0; k < Kc; ++k)  // the workers' slots are free (they took psi of step it - WR * NW)
-        if (u >= WR) mb_wait(&wempty[(k * NW + w0) * WR + wslot], ((u / WR) - 1) & 1);
+      if (u >= WR) {  // the workers' slots are free (they took psi of step it - WR * NW)
+        const unsigned par = ((u / WR) - 1) & 1;
+        if (Kc == 2)
+          mb_wait2(&wempty[w0 * WR + wslot], par, &wempty[(NW + w0) * WR + wslot], par);
+        else
+          for (int k = 0; k < Kc; ++k) mb_wait(&wempty[(k * NW + w0) * WR + wslot], par);
+      }
       const int slot = it % RING, use = it / RING;
       if (lpsi && use > 0) mb_wait(&pempty[slot], (use - 1) & 1);
       if (trc && tl == 0) trc[2] = clock64();
@@ -1134,8 +1149,13 @@ __global__ void __launch_bounds__(192, 1) lg_k_wsc_backward(const __grid_constan
       const int w0 = it % NW, u = it / NW, wslot = u % WR;
       long long* trc = (E.trace && si < 2) ? E.trace + (((long)g * 8 + 6 - si) * N + it) * 4 : nullptr;
       if (trc && tl == 0) trc[0] = clock64();
-      for (int k = 0; k < Kc; ++k)
-        if (u >= WR) mb_wait(&lempty[(k * NW + w0) * WR + wslot], ((u / WR) - 1) & 1);
+      if (u >= WR) {
+        const unsigned par = ((u / WR) - 1) & 1;
+        if (Kc == 2)
+          mb_wait2(&lempty[w0 * WR + wslot], par, &lempty[(NW + w0) * WR + wslot], par);
+        else
+          for (int k = 0; k < Kc; ++k) mb_wait(&lempty[(k * NW + w0) * WR + wslot], par);
+      }
       if (trc && tl == 0) trc[1] = clock64();
       if (i < d) {
         ws_sm[tb0 + i] = cur[0][0];
