@@ -543,8 +543,10 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
         team_chain_dense_w<W>(tm, cur[0][0], L.aop + (n & 1) * dd, pl.x, pl.y, 1.0, tb0, tb1, rt);
       else
         team_chain<W, 1, 1>(tm, cur, a, col, ac, accol, pl.x, pl.y, 1.0, tb0, tb1, rt, false);
-      const int slot = n % RING, use = n / RING;
-      if (use > 0) mb_wait(&empty[slot], (use - 1) & 1);
+      const int slot = n % RING;
+      // one slot-free wait per two steps: the scalars team consumes the ring in order, so its release
+      // of step n - 3 (slot (n + 1) % RING) implies step n - 4's (slot n % RING)
+      if ((n & 1) == 0 && n + 1 >= RING) mb_wait(&empty[(n + 1) % RING], (((n + 1) / RING) - 1) & 1);
       if (i < d) {
         ws_sm[L.ring + slot * d + i] = cur[0][0];
         ws_sm[tb0 + i] = cur[0][0];
