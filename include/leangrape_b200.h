@@ -187,6 +187,9 @@ int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms_per_launch);
 
 /* "<engine>:<dominant backward kernel>" chosen for this problem (diagnostics, bench.py roofline). */
 const char* lg_engine_name(lg_problem* p);
+/* Device state vectors held per trajectory by this problem's engine (GradientResult.live_vector_peak,
+ * src/costs.py:171-199); the same value lg_eval reports, also for sharded problems. */
+int64_t lg_live_vector_peak(lg_problem* p);
 /* Kernels launched by this library since load (all problems, all threads; diagnostics). */
 int64_t lg_launch_count(void);
 int lg_device_count(void);

@@ -126,6 +126,8 @@ def load() -> C.CDLL:
     lib.lg_device_count.argtypes = []
     lib.lg_engine_name.argtypes = [P]
     lib.lg_engine_name.restype = C.c_char_p
+    lib.lg_live_vector_peak.argtypes = [P]
+    lib.lg_live_vector_peak.restype = C.c_int64
     lib.lg_launch_count.argtypes = []
     lib.lg_launch_count.restype = C.c_int64
     lib.lg_last_error.restype = C.c_char_p

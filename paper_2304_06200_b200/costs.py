@@ -28,7 +28,7 @@ from enum import Enum
 import numpy as np
 
 from . import _native
-from .sparse import DenseMatrix, is_hermitian, one_norm_host, to_dense
+from .sparse import DenseMatrix, as_own_matrix, frozen_copy, is_hermitian, one_norm_host, to_dense
 
 __all__ = [
     "Backend",
@@ -116,7 +116,13 @@ class ControlProblem:
     basis: tuple | None = None
 
     def __post_init__(self):
-        object.__setattr__(self, "h_controls", tuple(self.h_controls))
+        # immutable private copies (device problems are cached per object, _native_for)
+        object.__setattr__(self, "h_static", as_own_matrix(self.h_static))
+        object.__setattr__(self, "h_controls", tuple(as_own_matrix(h) for h in self.h_controls))
+        if self.initial_state is not None:
+            object.__setattr__(self, "initial_state", frozen_copy(self.initial_state, np.complex128))
+        if self.basis is not None:
+            object.__setattr__(self, "basis", frozen_copy(np.asarray(self.basis), np.complex128))
         tol = 1e-12 * max(1.0, one_norm_host(self.h_static))
         if not is_hermitian(self.h_static, tol):
             raise ValueError("static Hamiltonian is not Hermitian within tolerance")
@@ -149,6 +155,12 @@ class CostTerm:
     def __post_init__(self):
         if self.weight < 0.0:
             raise ValueError("cost weights must be non-negative")
+        for name in ("target_state", "target_gate", "target_images"):
+            v = getattr(self, name)
+            if v is not None:
+                object.__setattr__(self, name, frozen_copy(v, np.complex128))
+        if self.penalty_op is not None:
+            object.__setattr__(self, "penalty_op", as_own_matrix(self.penalty_op))
         if self.kind in (CostKind.STATE_INFIDELITY, CostKind.STATE_RUNNING_INFIDELITY):
             if self.target_state is None:
                 raise ValueError(f"{self.kind.value} requires target_state")
@@ -377,7 +389,8 @@ class NativeProblem:
         cb = _native.ALLREDUCE_FN(lambda ptr, count, stream, user: hook(ptr, count))
         _native.check(self._lib.lg_eval_sharded(self.handle, a.n_steps, float(a.dt), _native.dptr(amps), cb, None,
                                                 C.byref(cost), _native.dptr(g)))
-        return GradientResult(cost=float(cost.value), grad=g, live_vector_peak=0)
+        return GradientResult(cost=float(cost.value), grad=g,
+                              live_vector_peak=int(self._lib.lg_live_vector_peak(self.handle)))
 
     def cost_sharded(self, a: ControlField, hook) -> float:
         amps = np.ascontiguousarray(a.amplitudes, np.float64)

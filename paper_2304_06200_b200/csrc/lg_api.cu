@@ -355,6 +355,8 @@ int lg_set_stream(lg_problem* p, void* stream) {
 
 int64_t lg_launch_count(void) { return g_launches; }
 
+int64_t lg_live_vector_peak(lg_problem* p) { return p ? (int64_t)p->live_peak : 0; }
+
 const char* lg_engine_name(lg_problem* p) {
   if (!p) return "none";
   switch (p->engine) {

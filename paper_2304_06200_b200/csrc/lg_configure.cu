@@ -598,7 +598,7 @@ int configure(lg_problem* p) {
   p->d_scratch = p->mem.alloc<double2>((size_t)p->scratch_per_group * p->n_groups);
   p->d_bar = p->mem.alloc<unsigned>(4 * (size_t)std::max(p->n_groups, 1));
   p->d_red = p->mem.alloc<double2>((size_t)2 * p->red_cap * p->n_slabs * std::max(p->n_groups, 1));
-  if (!p->d_scratch || !p->d_bar || !p->d_red) return fail(LG_CUDA_ERROR, "device allocation failed (scratch)");
+  if (p->mem.failed) return fail(LG_CUDA_ERROR, "device allocation failed (scratch)");
   return LG_OK;
 }
 

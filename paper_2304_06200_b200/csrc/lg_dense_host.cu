@@ -210,13 +210,13 @@ int configure_dense(lg_problem* p) {
   p->dd_xtb1 = M.alloc<double2>((size_t)cx * d);
   p->dd_tmp = M.alloc<double2>((size_t)Tmax * d);
   p->dd_dots = M.alloc<double2>((size_t)std::max<long>(64, (long)Imax * p->Kc * Tmax + 2 * cst));
-  if (!p->dd_dots || !p->dd_xtb1 || !p->d_Ai) return fail(LG_CUDA_ERROR, "device allocation failed (dense engine)");
   p->engine = 3;
   p->n_groups = 0;
   p->live_peak = (int)((3 * cst + 3 * cx + Tmax - 1) / Tmax);
   p->d_bar = M.alloc<unsigned>(4);
   p->d_scratch = M.alloc<double2>(1);
   p->d_red = M.alloc<double2>(1);
+  if (M.failed) return fail(LG_CUDA_ERROR, "device allocation failed (dense engine)");
   return LG_OK;
 }
 

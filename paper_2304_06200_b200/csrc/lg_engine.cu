@@ -524,13 +524,6 @@ extern "C" __global__ void lg_k_trsum(const double2* trp, int n_specs, int N, in
   trsum[q] = acc;
 }
 
-// cost and gradient from the raw per-trajectory scalars (lg_final.cuh).
-extern "C" __global__ void lg_k_finalize(const __grid_constant__ LgFinalArgs F) {
-  for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < (long)F.N * F.Kc; q += (long)gridDim.x * blockDim.x)
-    F.grad[q] = lg_final_grad(F, q);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *F.cost = lg_final_cost(F);
-}
-
 // explicit instantiations with C linkage-friendly wrappers
 extern "C" void* lg_forward_kernel(int multi) {
   return multi ? (void*)lg_k_forward<true> : (void*)lg_k_forward<false>;
@@ -539,4 +532,3 @@ extern "C" void* lg_backward_kernel(int multi) {
   return multi ? (void*)lg_k_backward<true> : (void*)lg_k_backward<false>;
 }
 extern "C" void* lg_trsum_kernel() { return (void*)lg_k_trsum; }
-extern "C" void* lg_finalize_kernel() { return (void*)lg_k_finalize; }

@@ -1,6 +1,9 @@
 // Cost and gradient from the raw per-trajectory scalars of the two sweeps.
 // Shared by the device finalize kernel and the host (sharded/multi-rank
-// combine, lg_finalize_host) so both produce identical numbers.
+// combine, lg_finalize_host) so both produce identical numbers: the kernel is
+// built in a -fmad=false unit (lg_prep.cu) and the host with -ffp-contract=off,
+// and |z| is numpy's formula (lg_np_cabs: one correctly rounded division, fma,
+// sqrt) on both sides instead of the two sides' different hypot().
 //
 // Per cost term s over its trajectory set t in [t0, t0 + K):
 //   STATE_INFIDELITY   cost 1/K sum_t (1 - |z_t|^2),  z_t = <psi_N|phi_t>     (src/costs.py:299-304)
@@ -63,7 +66,7 @@ LG_HD inline double lg_final_cost(const LgFinalArgs& F) {
     if (kind == LGK_STATE_INF) {
       for (int t = 0; t < K; ++t) {
         const double2 z = F.fin[(long)s * T + t0 + t];
-        const double a = hypot(z.x, z.y);
+        const double a = lg_np_cabs(z.x, z.y);
         cs += 1.0 - a * a;
       }
       cs /= K;
@@ -76,7 +79,7 @@ LG_HD inline double lg_final_cost(const LgFinalArgs& F) {
     } else if (kind == LGK_GATE) {
       double tx = 0.0, ty = 0.0;
       for (int t = 0; t < K; ++t) tx += F.fin[(long)s * T + t0 + t].x, ty += F.fin[(long)s * T + t0 + t].y;
-      const double a = hypot(tx, ty);
+      const double a = lg_np_cabs(tx, ty);
       cs = 1.0 - a * a / ((double)K * K);
     } else {
       double acc = 0.0;
@@ -86,7 +89,7 @@ LG_HD inline double lg_final_cost(const LgFinalArgs& F) {
           const double2 v = F.trp[((long)s * N + n) * T + t0 + t];
           tx += v.x, ty += v.y;
         }
-        const double a = hypot(tx, ty);
+        const double a = lg_np_cabs(tx, ty);
         acc += a * a;
       }
       cs = 1.0 - acc / ((double)N * K * K);

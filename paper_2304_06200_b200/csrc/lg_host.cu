@@ -142,7 +142,10 @@ int prepare_dt(lg_problem* p, double dt) {
   p->d_ac_rowlen = p->dtmem.upload(acrow);
   p->d_ac_abs = acabs.empty() ? nullptr : p->dtmem.upload(acabs);
   p->d_ac_abs_dense = acabs_dense.empty() ? nullptr : p->dtmem.upload(acabs_dense);
-  if (!p->d_Ac || !p->d_ctrl_col) return fail(LG_CUDA_ERROR, "device allocation failed (per-dt data)");
+  if (p->dtmem.failed) {
+    p->dtmem.release();
+    return fail(LG_CUDA_ERROR, "device allocation failed (per-dt data)");
+  }
   p->cached_dt = dt;
   return LG_OK;
 }
@@ -181,7 +184,11 @@ int ensure_N(lg_problem* p, long N) {
   }
   p->d_spec_t0 = m.upload(st0);
   p->d_spec_K = m.upload(sK);
-  if (!p->d_cost || !p->d_A || !p->d_spec_K) return fail(LG_CUDA_ERROR, "device allocation failed (per-step buffers)");
+  if (m.failed) {  // every buffer or none: a partial set would leave null pointers for the kernels
+    m.release();
+    p->capN = 0;
+    return fail(LG_CUDA_ERROR, "device allocation failed (per-step buffers)");
+  }
   p->capN = N;
   return LG_OK;
 }
@@ -433,7 +440,10 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
   p->dense = p->hs.dense;
   for (auto& m : p->hc) p->dense = p->dense || m.dense;
   p->materialise = 2 * d <= 256;  // src/derivatives.py:29,199-202
-  p->dense_large = p->dense && d > 512;  // per-term DMMA GEMM engine (lg_dense.cu)
+  // per-term DMMA GEMM engine (lg_dense.cu); LG_ENGINE=dense forces it for smaller dense problems
+  // (tests exercise its kernels against the dense goldens below d = 512)
+  const char* fe = std::getenv("LG_ENGINE");
+  p->dense_large = p->dense && D->backend == 0 && (d > 512 || (fe && std::string(fe) == "dense"));
   // ---- terms and trajectory sets
   if (D->n_terms > LG_MAX_SPECS) return fail(LG_UNSUPPORTED, "more than 8 cost terms");
   bool has_state = false, has_gate = false;
@@ -642,8 +652,10 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
       sp.d_tgt = M.upload(sp.tgt);
     }
   }
-  if (!p->d_traj || !p->d_cols) return fail(LG_CUDA_ERROR, "device allocation failed (problem data)");
-  return configure(p);
+  if (M.failed) return fail(LG_CUDA_ERROR, "device allocation failed (problem data)");
+  const int rc_cfg = configure(p);
+  if (rc_cfg == LG_OK && p->mem.failed) return fail(LG_CUDA_ERROR, "device allocation failed (engine buffers)");
+  return rc_cfg;
 }
 
 }  // namespace lgi

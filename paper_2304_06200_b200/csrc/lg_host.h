@@ -72,11 +72,16 @@ inline double2 gen_host(double2 h, double dt) { return make_double2(dt * h.y, -(
 
 struct DevMem {
   std::vector<void*> ptrs;
+  bool failed = false;  // some alloc() since the last release() failed: callers check this once
   template <class T>
   T* alloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();  // clear the (non-sticky) allocation error
+      failed = true;
+      return nullptr;
+    }
     ptrs.push_back(p);
     return (T*)p;
   }
@@ -89,6 +94,7 @@ struct DevMem {
   void release() {
     for (void* p : ptrs) cudaFree(p);
     ptrs.clear();
+    failed = false;
   }
 };
 

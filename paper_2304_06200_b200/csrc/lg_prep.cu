@@ -10,6 +10,7 @@
 //
 // This translation unit is compiled with -fmad=false: the arithmetic below
 // must round exactly like numpy (see lg_numpy.cuh).
+#include "lg_final.cuh"
 #include "lg_numpy.cuh"
 #include "lg_planner.cuh"
 #include "lg_types.h"
@@ -324,3 +325,12 @@ extern "C" __global__ void lg_k_rtab(const int4* plan, int Kc, int N, double* rt
 }
 extern "C" void* lg_rtab_kernel() { return (void*)lg_k_rtab; }
 extern "C" void* lg_gather_kernel() { return (void*)lg_k_gather_plan_inputs; }
+
+// cost and gradient from the raw per-trajectory scalars (lg_final.cuh).  Built here, in the
+// -fmad=false unit, so it rounds exactly like the host combine lg_finalize_host.
+extern "C" __global__ void lg_k_finalize(const __grid_constant__ LgFinalArgs F) {
+  for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < (long)F.N * F.Kc; q += (long)gridDim.x * blockDim.x)
+    F.grad[q] = lg_final_grad(F, q);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *F.cost = lg_final_cost(F);
+}
+extern "C" void* lg_finalize_kernel() { return (void*)lg_k_finalize; }

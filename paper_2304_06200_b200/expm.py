@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native
 
-__all__ = ["ExpmPlan", "PlanningError", "make_plan", "make_plans_device", "plan_inputs", "apply", "expm_multiply",
+__all__ = ["ExpmPlan", "PlanningError", "BoundInfeasibleError", "make_plan", "make_plans_device", "plan_inputs", "apply", "expm_multiply",
            "is_anti_hermitian", "DEFAULT_M_MAX", "DEFAULT_S_MAX"]
 
 DEFAULT_M_MAX = 60
@@ -25,6 +25,12 @@ DEFAULT_S_MAX = 10_000
 
 class PlanningError(RuntimeError):
     """No feasible (order, scaling) pair within the search limits."""
+
+
+class BoundInfeasibleError(ArithmeticError):
+    """The rounding model is outside its validity range (n u' >= 1, src/expm.py:65-67,146-153).
+    The planner handles it internally (such plans are skipped, as the reference's loop does);
+    exported for API parity."""
 
 
 @dataclass(frozen=True)

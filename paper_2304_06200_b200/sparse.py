@@ -31,11 +31,21 @@ __all__ = [
     "kron_csr",
     "is_hermitian",
     "to_dense",
+    "frozen_copy",
+    "as_own_matrix",
 ]
 
 
 class SparseMatrixError(ValueError):
     """Malformed construction input or shape mismatch (src/sparse.py:37-38)."""
+
+
+def frozen_copy(a, dtype=None, order="C"):
+    """A private read-only copy: device problems are cached per Python object, so the arrays an
+    object describes must not change behind the cache (in-place edits raise instead)."""
+    out = np.array(a, dtype=dtype, order=order, copy=True)
+    out.setflags(write=False)
+    return out
 
 
 @dataclass(frozen=True, eq=False)
@@ -46,6 +56,11 @@ class CsrMatrix:
     col_indices: np.ndarray
     values: np.ndarray
 
+    def __post_init__(self):
+        object.__setattr__(self, "row_offsets", frozen_copy(self.row_offsets, np.int64))
+        object.__setattr__(self, "col_indices", frozen_copy(self.col_indices, np.int64))
+        object.__setattr__(self, "values", frozen_copy(self.values, np.complex128))
+
     @property
     def nnz(self) -> int:
         return int(self.values.size)
@@ -53,6 +68,40 @@ class CsrMatrix:
     @property
     def shape(self):
         return (self.n_rows, self.n_cols)
+
+    # --- host-side descriptors with the reference's semantics (src/sparse.py:90-133); validation
+    # and planning helpers, not the hot path (every matvec of an evaluation runs fused on the GPU)
+    def col_abs_sums(self) -> np.ndarray:
+        return np.bincount(self.col_indices, weights=np.abs(self.values), minlength=self.n_cols)
+
+    def row_abs_sums(self) -> np.ndarray:
+        sums = np.zeros(self.n_rows)
+        if self.nnz:
+            sums = np.add.reduceat(np.abs(self.values), np.minimum(self.row_offsets[:-1], self.nnz - 1))
+            sums[self.row_offsets[:-1] == self.row_offsets[1:]] = 0.0
+        return sums
+
+    def row_nnz_counts(self) -> np.ndarray:
+        return np.diff(self.row_offsets)
+
+    def one_norm(self) -> float:
+        return 0.0 if self.nnz == 0 else float(self.col_abs_sums().max())
+
+    def inf_norm(self) -> float:
+        return 0.0 if self.nnz == 0 else float(self.row_abs_sums().max())
+
+    def max_row_nnz(self) -> int:
+        return 0 if self.n_rows == 0 else int(self.row_nnz_counts().max())
+
+    def scaled(self, factor: complex) -> "CsrMatrix":
+        if factor == 0:
+            return build_csr([], self.n_rows, self.n_cols)
+        return CsrMatrix(self.n_rows, self.n_cols, self.row_offsets, self.col_indices, self.values * complex(factor))
+
+    def matvec(self, v, out=None):
+        raise NotImplementedError(
+            "CsrMatrix.matvec: the product runs matvecs only fused inside the GPU sweeps "
+            "(composite_grad / composite_cost / expm.apply); there is no host matvec (no CPU fallback)")
 
     def triplets(self):
         rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_offsets))
@@ -74,7 +123,7 @@ class DenseMatrix:
     array: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        arr = np.asfortranarray(np.asarray(self.array, dtype=np.complex128))
+        arr = frozen_copy(self.array, np.complex128, order="F")
         if arr.ndim != 2:
             raise SparseMatrixError("DenseMatrix expects a 2-d array")
         if not np.isfinite(arr).all():
@@ -96,6 +145,33 @@ class DenseMatrix:
     @property
     def nnz(self):
         return self.array.size
+
+    # --- host-side descriptors (src/sparse.py:201-227); Dense max_row_nnz is n_cols (:220-222)
+    def col_abs_sums(self) -> np.ndarray:
+        return np.abs(self.array).sum(axis=0)
+
+    def row_abs_sums(self) -> np.ndarray:
+        return np.abs(self.array).sum(axis=1)
+
+    def row_nnz_counts(self) -> np.ndarray:
+        return np.full(self.n_rows, self.n_cols, dtype=np.int64)
+
+    def one_norm(self) -> float:
+        return float(self.col_abs_sums().max()) if self.array.size else 0.0
+
+    def inf_norm(self) -> float:
+        return float(self.row_abs_sums().max()) if self.array.size else 0.0
+
+    def max_row_nnz(self) -> int:
+        return int(self.n_cols)
+
+    def scaled(self, factor: complex) -> "DenseMatrix":
+        return DenseMatrix(self.array * complex(factor))
+
+    def matvec(self, v, out=None):
+        raise NotImplementedError(
+            "DenseMatrix.matvec: the product runs matvecs only fused inside the GPU sweeps "
+            "(composite_grad / composite_cost / expm.apply); there is no host matvec (no CPU fallback)")
 
     def to_dense(self) -> np.ndarray:
         return self.array.copy(order="F")
@@ -144,6 +220,15 @@ def from_dense(array) -> CsrMatrix:
 def identity_csr(n: int) -> CsrMatrix:
     i = np.arange(n, dtype=np.int64)
     return build_csr_arrays(i, i, np.ones(n, np.complex128), n, n)
+
+
+def as_own_matrix(m):
+    """This package's (immutable) matrix type for any object with the reference's field names."""
+    if isinstance(m, (CsrMatrix, DenseMatrix)):
+        return m
+    if hasattr(m, "array"):
+        return DenseMatrix(m.array)
+    return CsrMatrix(int(m.n_rows), int(m.n_cols), m.row_offsets, m.col_indices, m.values)
 
 
 def to_dense(m) -> np.ndarray:

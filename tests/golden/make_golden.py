@@ -351,6 +351,78 @@ def golden_c5(n_prefix=4, k_sub=4):
          cost=cost, grad=grad, hs_checksum=np.sum(np.abs(h_s.array)), **{"plan_" + k: v for k, v in pt.items()})
 
 
+def _c3_state(h):
+    """One state of the full-size c3 block (worker process)."""
+    h_s, hx, hy = tc_ops(6, 200)
+    amps = controls(103, 2000, 2, 0.01)
+    a = costs.ControlField(2000, 2, 0.5, amps)
+    pr = costs.ControlProblem(h_s, (hx, hy), initial_state=models.fock_state(1200, h))
+    r = costs.composite_grad(pr, a, [costs.CostTerm(costs.CostKind.STATE_INFIDELITY, 1.0,
+                                                    target_state=models.fock_state(1200, h + 1))])
+    return r.cost, r.grad
+
+
+def _c5_parts():
+    d = 4096
+    rng = np.random.default_rng(5005)
+    hs_arr, s1 = gue(rng, d, 1.0)
+    hc_arr, s2 = gue(rng, d, 0.1)
+    psi0s = rand_states(rng, 64, d)
+    phis = rand_states(rng, 64, d)
+    return sparse.DenseMatrix(hs_arr * s1), sparse.DenseMatrix(hc_arr * s2), psi0s, phis, s1, s2
+
+
+_C5 = None
+
+
+def _c5_state(arg):
+    """One state of the full-K c5 prefix (worker process; the matrices are built once per worker)."""
+    global _C5
+    h, n_prefix = arg
+    if _C5 is None:
+        _C5 = _c5_parts()
+    h_s, hc, psi0s, phis, _, _ = _C5
+    a = costs.ControlField(n_prefix, 1, 0.1, controls(105, 1000, 1, 1.0)[:n_prefix])
+    pr = costs.ControlProblem(h_s, (hc,), initial_state=psi0s[h])
+    r = costs.composite_grad(pr, a, [costs.CostTerm(costs.CostKind.STATE_INFIDELITY, 1.0, target_state=phis[h])])
+    return r.cost, r.grad
+
+
+def _pool(fn, items, procs=8):
+    import multiprocessing as mp
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    with mp.get_context("fork").Pool(procs) as pool:
+        return pool.map(fn, items, chunksize=1)
+
+
+def golden_c3_full():
+    """config 3 at FULL size (N=2000, K=8): the reference's composite_grad per state, one process
+    per state, summed in state order exactly as ref_state_block does (c_tot += cost/K)."""
+    t0 = time.time()
+    parts = _pool(_c3_state, list(range(8)))
+    cost, grad = 0.0, np.zeros((2000, 2))
+    for c, g in parts:
+        cost += c / 8
+        grad += g / 8
+    print(f"c3 full: {time.time() - t0:.1f}s cost={cost}")
+    save("c3_full", cost=cost, grad=grad, state_costs=np.array([c for c, _ in parts]))
+
+
+def golden_c5_fullk(n_prefix=2):
+    """config 5 with ALL K=64 states (the full-K dense GEMM path: 64/128-column Taylor terms), prefix
+    N' of N=1000; per-state composite_grad summed in state order."""
+    t0 = time.time()
+    parts = _pool(_c5_state, [(h, n_prefix) for h in range(64)])
+    cost, grad = 0.0, np.zeros((n_prefix, 1))
+    for c, g in parts:
+        cost += c / 64
+        grad += g / 64
+    print(f"c5 full-K prefix {n_prefix}: {time.time() - t0:.1f}s cost={cost}")
+    save("c5_fullk", cost=cost, grad=grad, n_prefix=np.int64(n_prefix),
+         state_costs=np.array([c for c, _ in parts]), state_grads=np.array([g for _, g in parts]))
+
+
 def golden_stress():
     """Random-state / large-amplitude variants with every cost kind (plans vary per step)."""
     out = {}

@@ -1,0 +1,80 @@
+"""GPU parity at BASELINE's full sizes where the reference finishes in minutes.
+
+* c3 at full size (N=2000, K=8): golden ``c3_full.npz`` = the reference's composite_grad per state
+  (src/costs.py:515-546 -> _state_pass :269-354), summed in state order (make_golden.py).
+* c5 with ALL K=64 states on an N'=2 prefix: the full-K dense engine path.  Its forward chain has
+  64 columns and its adjoint / aux chains 128 / 64, so every Taylor GEMM runs the wide-tile kernel
+  ``lg_k_zgemm_taylor_n32`` with split-k 8 (lg_dense_host.cu: chosen from 64 columns) -- the
+  kernel every full-size c5 evaluation executes (DenseMatrix.matvec, src/sparse.py:193-199, inside
+  expm.apply, src/expm.py:345-350).
+* The same dense cases with the wide tile forced from 1 column (LG_ZGEMM_N32=1) and with split-k
+  forced off / to 8, so both GEMM kernels and the split-k epilogue meet every dense golden.
+
+Bars: cost within 1e-12 absolute, gradient within 1e-9 relative (norm-wise).
+"""
+
+import numpy as np
+import pytest
+
+import _golden as G
+from paper_2304_06200_b200 import ControlField, ControlProblem, CostKind, CostTerm, composite_grad, models
+from paper_2304_06200_b200.costs import NativeProblem
+
+pytestmark = pytest.mark.gpu
+
+COST_TOL = 1e-12
+GRAD_TOL = 1e-9
+
+
+def _check(res, cost, grad):
+    assert abs(res.cost - float(cost)) <= COST_TOL, (res.cost, float(cost))
+    assert G.grad_rel(res.grad, grad) <= GRAD_TOL, G.grad_rel(res.grad, grad)
+
+
+def test_c3_full_size_against_reference():
+    z = G.load("c3_full")
+    case = models.build_case("c3")
+    _check(composite_grad(case.problem, case.field, case.terms), z["cost"], z["grad"])
+
+
+def test_c5_all_64_states_full_k_gemm_path():
+    z = G.load("c5_fullk")
+    n = int(z["n_prefix"])
+    case = models.build_case("c5", n_steps=n, n_states=64)
+    npb = NativeProblem(case.problem, case.terms, initial_states=case.problem.initial_state)
+    assert npb.engine.startswith("dense"), npb.engine
+    res = npb.grad(case.field)
+    _check(res, z["cost"], z["grad"])
+    # per-trajectory raw scalars: the final overlaps <psi_N|phi_t> of all 64 states reproduce each
+    # state's reference cost 1 - |<phi|psi_N>|^2 individually
+    assert abs(npb.cost(case.field) - float(z["cost"])) <= COST_TOL
+
+
+@pytest.mark.parametrize("n32,splitk", [("1", None), ("1", "1"), ("0", "8"), ("1", "8")])
+def test_dense_goldens_with_forced_gemm_tiles(n32, splitk, monkeypatch):
+    monkeypatch.setenv("LG_ZGEMM_N32", n32)
+    if splitk:
+        monkeypatch.setenv("LG_SPLITK", splitk)
+    z = G.load("c5")
+    case = models.build_case("c5", n_steps=int(z["amps"].shape[0]), n_states=int(z["k_sub"]))
+    _check(NativeProblem(case.problem, case.terms, initial_states=case.problem.initial_state).grad(case.field),
+           z["cost"], z["grad"])
+    # the dense stress variant (d = 160, all five cost kinds, +-1 rad/ns controls: plans vary per
+    # step) on the dense GEMM engine (LG_ENGINE=dense; it otherwise takes d > 512 only)
+    monkeypatch.setenv("LG_ENGINE", "dense")
+    zs = G.sub(G.load("stress"), "s_denseblk160")
+    hs, hc = G.mats(zs)
+    om = G.penalty(zs)
+    N, Kc = zs["amps"].shape
+    a = ControlField(N, Kc, float(zs["dt"]), zs["amps"])
+    prob = ControlProblem(hs, tuple(hc), initial_state=zs["psi0"], basis=zs["basis"])
+    terms = [CostTerm(CostKind.STATE_INFIDELITY, 0.7, target_state=zs["targets"]),
+             CostTerm(CostKind.STATE_PENALTY, 0.2, penalty_op=om),
+             CostTerm(CostKind.STATE_RUNNING_INFIDELITY, 0.4, target_state=zs["targets"])]
+    npb = NativeProblem(prob, terms, initial_states=zs["psi0"])
+    assert npb.engine.startswith("dense"), npb.engine
+    _check(npb.grad(a), zs["cost_state"], zs["grad_state"])
+    for kind, ck, gk in [(CostKind.GATE_INFIDELITY, "cost_g1", "grad_g1"),
+                         (CostKind.GATE_RUNNING_INFIDELITY, "cost_g3", "grad_g3")]:
+        t = [CostTerm(kind, 1.0, target_images=zs["images"])]
+        _check(NativeProblem(prob, t, basis=zs["basis"]).grad(a), zs[ck], zs[gk])

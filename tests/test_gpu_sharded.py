@@ -93,6 +93,7 @@ def test_sharded_matches_unsharded_bitwise(tag):
     r1 = ev.grad(a)
     assert ev.calls == 3  # running gate traces between the sweeps + (ip|fin) + run
     assert r1.cost == ref.cost and np.array_equal(r1.grad, ref.grad)
+    assert r1.live_vector_peak == ref.live_vector_peak > 0
     assert ev.cost(a) == ref_cost and ev.calls == 1
     # two shards on two host threads
     world = 2
@@ -124,3 +125,16 @@ def test_unhooked_sharded_running_gate_is_refused():
     npb = NativeProblem(prob, terms, prob.initial_state, prob.basis, shard=(0, 1))
     with pytest.raises(NotImplementedError):
         npb.grad(a)
+
+
+@pytest.mark.parametrize("tag", ["s_csr60", "s_block160", "s_denseblk160"])
+def test_host_combine_of_raw_scalars_is_bitwise_the_device_combine(tag):
+    """lg_raw_get + lg_finalize_host (the multi-rank combine) == lg_eval bit for bit:
+    lg_k_finalize is built -fmad=false and both sides share lg_final.cuh (numpy's |z|)."""
+    z, a, prob, terms = _setup(tag)
+    terms = terms[:4]  # no running gate term: a plain lg_eval works on any problem
+    npb = NativeProblem(prob, terms, prob.initial_state, prob.basis)
+    res = npb.grad(a)
+    cost, grad = npb.finalize(a.n_steps, npb.raw(a.n_steps))
+    assert cost == res.cost
+    assert np.array_equal(grad, res.grad)
