@@ -314,25 +314,23 @@ int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms) {
   tmp.d = d;
   CK(cudaStreamCreate(&tmp.stream));
   DevMem m;
-  double* Ar = m.alloc<double>((size_t)d * d);
-  double* Ai = m.alloc<double>((size_t)d * d);
+  double2* Ad = m.alloc<double2>((size_t)d * d);
   double2* X = m.alloc<double2>((size_t)d * C);
   double2* cur = m.alloc<double2>((size_t)d * C);
   double2* T = m.alloc<double2>((size_t)d * C);
-  if (!Ar || !Ai || !X || !cur || !T) {
+  if (m.failed) {
     m.release();
     return fail(LG_CUDA_ERROR, "allocation failed");
   }
-  cudaMemset(Ar, 0, sizeof(double) * d * d);
-  cudaMemset(Ai, 0, sizeof(double) * d * d);
+  cudaMemset(Ad, 0, sizeof(double2) * d * d);
   cudaMemset(X, 0, sizeof(double2) * d * C);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   int rc = LG_OK;
-  for (int it = 0; it < 3 && !rc; ++it) rc = dense_gemm(&tmp, Ar, Ai, X, nullptr, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
+  for (int it = 0; it < 3 && !rc; ++it) rc = dense_gemm(&tmp, Ad, X, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
   cudaEventRecord(e0, tmp.stream);
-  for (int it = 0; it < iters && !rc; ++it) rc = dense_gemm(&tmp, Ar, Ai, X, nullptr, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
+  for (int it = 0; it < iters && !rc; ++it) rc = dense_gemm(&tmp, Ad, X, nullptr, nullptr, C, 0.5, false, false, nullptr, cur, T);
   cudaEventRecord(e1, tmp.stream);
   cudaEventSynchronize(e1);
   float t = 0.f;

@@ -5,26 +5,31 @@
 // pipe (mma.sync.aligned.m8n8k4.f64 -> SASS DMMA; sm_100a has no tcgen05 f64
 // kind), with the Taylor scale-and-accumulate fused into the epilogue:
 //     t = (A X) (sgn / (s j));  cur += t;  T_out = last ? cur : t.
-// A is stored planar (Ar, Ai), column-major; X / cur / T are interleaved
-// double2, column-major (column = one state vector).  The complex product uses
-// three real MMAs per fragment pair (the 3M / Gauss scheme of ZGEMM3M):
+// A, X, cur and T are interleaved complex (double2), column-major (a column of
+// X = one state vector).  The complex product uses three real MMAs per
+// fragment pair (the 3M / Gauss scheme of ZGEMM3M):
 //     T1 += Ar Xr,  T2 += Ai Xi,  T3 += (Ar + Ai)(Xr + Xi);
 //     Yr = T1 - T2,  Yi = T3 - T1 - T2,
-// with the operand sums formed from the fragments already in registers, so the
-// tensor pipe does 3/4 of the 4M work at the same operand traffic.  (Norm-wise
-// error of 3M is a small multiple of the 4M bound -- Higham, "Stability of a
-// method for multiplying complex matrices with three real matrix
-// multiplications" -- far inside the parity tolerances.)
-// An operand may be the concatenation of two segments (the aux embedding's
-// top block [A | A_c] [top; bottom], src/derivatives.py:154-164).
+// with the operand sums formed from the fragments in registers, so the tensor
+// pipe does 3/4 of the 4M work at the same operand traffic.  (Norm-wise error
+// of 3M is a small multiple of the 4M bound -- Higham, "Stability of a method
+// for multiplying complex matrices with three real matrix multiplications" --
+// far inside the parity tolerances.)
+// Tiles move global -> shared by cp.async (16-byte complex elements, zero-fill
+// past the edges), double-buffered, with no register staging; both tiles keep
+// the interleaved layout so one LDS.128 yields (re, im) of a fragment element,
+// and the row strides (A: BM + 2, X: BK + 4 complex) make every quarter-warp's
+// fragment loads and every cp.async store bank-conflict-free.
+// An operand may be the concatenation of two segments (the aux embedding's top
+// block [A | A_c] [top; bottom], src/derivatives.py:154-164).
 #include <cuda_runtime.h>
 
 #include "lg_types.h"
 
 namespace {
 
-constexpr int BM = 64, BK = 16, SA = BM + 8;
-extern __shared__ __align__(16) double zg_dsm[];
+constexpr int BM = 64, BK = 16, SAM = BM + 2, SXK = BK + 4;
+extern __shared__ __align__(16) double2 zg_dsm[];
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -32,28 +37,28 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+// 16-byte async copy; src_bytes = 0 zero-fills the destination (tile edges)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 }  // namespace
 
-
-
 // grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x BN tile,
 // BN = 8 NTT columns (NTT = 2 or 4: the wider tile halves the A-fragment loads per DMMA).
-// Dynamic shared memory: zgemm_smem_bytes(NTT).
+// Dynamic shared memory: lg_zgemm_smem_bytes(NTT).
 template <int NTT>
 __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
-  constexpr int BN = 8 * NTT, SX = BN + 1;
-  auto sAr = reinterpret_cast<double(*)[BK][SA]>(zg_dsm);
-  auto sAi = reinterpret_cast<double(*)[BK][SA]>(zg_dsm + 2 * BK * SA);
-  auto sXr = reinterpret_cast<double(*)[BK][SX]>(zg_dsm + 4 * BK * SA);
-  auto sXi = reinterpret_cast<double(*)[BK][SX]>(zg_dsm + 4 * BK * SA + 2 * BK * SX);
+  constexpr int BN = 8 * NTT;
+  constexpr int A_ST = BK * SAM, X_ST = BN * SXK;  // complex elements per stage
+  double2* sA = zg_dsm;              // [2][BK][SAM]
+  double2* sX = zg_dsm + 2 * A_ST;   // [2][BN][SXK]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q4 = lane & 3, r8 = lane >> 2;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int M = G.M, C = G.C;
   double t1[2][NTT][2], t2[2][NTT][2], t3[2][NTT][2];
@@ -65,83 +70,69 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
       for (int v = 0; v < 2; ++v) t1[a][b][v] = t2[a][b][v] = t3[a][b][v] = 0.0;
 
   // flattened k-tiles over the segments; this CTA's slice [t_lo, t_hi)
-  int tiles0 = (G.seg[0].K + BK - 1) / BK;
+  const int tiles0 = (G.seg[0].K + BK - 1) / BK;
   const int all_tiles = tiles0 + (G.nseg > 1 ? (G.seg[1].K + BK - 1) / BK : 0);
   const int t_lo = (int)((long)all_tiles * blockIdx.z / gridDim.z);
   const int t_hi = (int)((long)all_tiles * (blockIdx.z + 1) / gridDim.z);
   const int total = t_hi - t_lo;
-  const bool full_m = (m0 + BM <= M);
 
-  auto load_tile = [&](int tl, int buf, double2* xreg) {
+  auto load_tile = [&](int tl, int buf) {
     const int t = t_lo + tl;
     const LgGemmSeg& S = G.seg[t < tiles0 ? 0 : 1];
     const int k0 = (t < tiles0 ? t : t - tiles0) * BK;
-    // A: BK columns x BM rows per plane; 16-byte chunks: BK * BM / 2 per plane
+    double2* dA = sA + buf * A_ST;
+    double2* dX = sX + buf * X_ST;
+    // A: BK columns (k) x BM rows (m), consecutive threads on consecutive rows (coalesced)
 #pragma unroll
-    for (int q = 0; q < (BK * BM / 2) / 128; ++q) {
-      const int chunk = tid + q * 128;
-      const int kk = chunk / (BM / 2), mm = (chunk % (BM / 2)) * 2;
+    for (int q = 0; q < (BK * BM) / 128; ++q) {
+      const int e = tid + q * 128;
+      const int kk = e / BM, mm = e % BM;
       const int k = k0 + kk, m = m0 + mm;
-      if (k < S.K && full_m) {
-        cp_async16(&sAr[buf][kk][mm], S.Ar + (long)k * S.lda + m);
-        cp_async16(&sAi[buf][kk][mm], S.Ai + (long)k * S.lda + m);
-      } else {
-        for (int e = 0; e < 2; ++e) {
-          const bool ok = k < S.K && m + e < M;
-          sAr[buf][kk][mm + e] = ok ? S.Ar[(long)k * S.lda + m + e] : 0.0;
-          sAi[buf][kk][mm + e] = ok ? S.Ai[(long)k * S.lda + m + e] : 0.0;
-        }
-      }
+      const bool ok = k < S.K && m < M;
+      cp_async16(dA + kk * SAM + mm, ok ? S.A + (long)k * S.lda + m : S.A, ok ? 16 : 0);
     }
-    // X: BK x BN complex, into registers (stored to smem after the current compute)
+    // X: BN columns (n) x BK rows (k), consecutive threads on consecutive k of a column
 #pragma unroll
     for (int q = 0; q < (BK * BN) / 128; ++q) {
       const int e = tid + q * 128;
       const int nn = e / BK, kk = e % BK;
       const int k = k0 + kk, n = n0 + nn;
-      xreg[q] = (k < S.K && n < C) ? S.X[(long)n * S.ldx + k] : make_double2(0.0, 0.0);
+      const bool ok = k < S.K && n < C;
+      cp_async16(dX + nn * SXK + kk, ok ? S.X + (long)n * S.ldx + k : S.X, ok ? 16 : 0);
     }
     cp_async_commit();
   };
-  auto store_x = [&](int buf, const double2* xreg) {
-#pragma unroll
-    for (int q = 0; q < (BK * BN) / 128; ++q) {
-      const int e = tid + q * 128;
-      const int nn = e / BK, kk = e % BK;
-      sXr[buf][kk][nn] = xreg[q].x;
-      sXi[buf][kk][nn] = xreg[q].y;
-    }
-  };
 
-  double2 xreg[(BK * BN) / 128];
-  if (total > 0) {
-    load_tile(0, 0, xreg);
-    store_x(0, xreg);
-  }
+  if (total > 0) load_tile(0, 0);
   for (int t = 0; t < total; ++t) {
     const int buf = t & 1;
-    cp_async_wait0();
+    if (t + 1 < total) {
+      load_tile(t + 1, buf ^ 1);  // buffer buf ^ 1 was released by the barrier ending step t - 1
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
     __syncthreads();
-    if (t + 1 < total) load_tile(t + 1, buf ^ 1, xreg);
+    const double2* cA = sA + buf * A_ST + q4 * SAM + warp * 16 + r8;
+    const double2* cX = sX + buf * X_ST + r8 * SXK + q4;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      const int ka = kk + (lane & 3);
       double ar[2], ai[2], sa[2], xr[NTT], xi[NTT], sx[NTT];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
-        const int m = warp * 16 + mt * 8 + (lane >> 2);
-        ar[mt] = sAr[buf][ka][m];
-        ai[mt] = sAi[buf][ka][m];
-        sa[mt] = ar[mt] + ai[mt];
+        const double2 a = cA[kk * SAM + mt * 8];
+        ar[mt] = a.x;
+        ai[mt] = a.y;
+        sa[mt] = a.x + a.y;
       }
 #pragma unroll
       for (int nt = 0; nt < NTT; ++nt) {
-        const int n = nt * 8 + (lane >> 2);
-        xr[nt] = sXr[buf][ka][n];
-        xi[nt] = sXi[buf][ka][n];
-        sx[nt] = xr[nt] + xi[nt];
+        const double2 x = cX[nt * 8 * SXK + kk];
+        xr[nt] = x.x;
+        xi[nt] = x.y;
+        sx[nt] = x.x + x.y;
       }
-      // 12 independent DMMAs per k-step: each accumulator is updated once per step
+      // 3 x 2 x NTT independent DMMAs per k-step: each accumulator is updated once per step
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -155,10 +146,7 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
 #pragma unroll
         for (int nt = 0; nt < NTT; ++nt) dmma(t3[mt][nt][0], t3[mt][nt][1], sa[mt], sx[nt]);
     }
-    if (t + 1 < total) {
-      __syncthreads();  // everyone done reading sX[buf ^ 1] of tile t - 1
-      store_x(buf ^ 1, xreg);
-    }
+    __syncthreads();  // every warp done with buffer buf before tile t + 2 is copied into it
   }
   double yr[2][NTT][2], yi[2][NTT][2];
 #pragma unroll
@@ -178,8 +166,8 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
       for (int nt = 0; nt < NTT; ++nt)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
-          const int n = n0 + nt * 8 + 2 * (lane & 3) + v;
+          const int m = m0 + warp * 16 + mt * 8 + r8;
+          const int n = n0 + nt * 8 + 2 * q4 + v;
           if (m < M && n < C) P[(long)n * M + m] = make_double2(yr[mt][nt][v], yi[mt][nt][v]);
         }
     return;
@@ -192,8 +180,8 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
     for (int nt = 0; nt < NTT; ++nt)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int m = m0 + warp * 16 + mt * 8 + (lane >> 2);
-        const int n = n0 + nt * 8 + 2 * (lane & 3) + v;
+        const int m = m0 + warp * 16 + mt * 8 + r8;
+        const int n = n0 + nt * 8 + 2 * q4 + v;
         if (m >= M || n >= C) continue;
         const double2 tt = make_double2(yr[mt][nt][v] * r, yi[mt][nt][v] * r);
         double2 base;
@@ -213,7 +201,7 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid
 extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor_n32(const __grid_constant__ LgGemmArgs G) {
   zgemm_taylor<4>(G);
 }
-extern "C" int lg_zgemm_smem_bytes(int ntt) { return (int)sizeof(double) * (4 * BK * SA + 4 * BK * (8 * ntt + 1)); }
+extern "C" int lg_zgemm_smem_bytes(int ntt) { return (int)sizeof(double2) * 2 * (BK * SAM + 8 * ntt * SXK); }
 
 // Split-k finish: y = sum of the k-slices in slice order (deterministic), then the Taylor update.
 extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G) {
@@ -238,10 +226,10 @@ extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G)
   }
 }
 
-// A_n = -i dt (H_s + sum_c a_c h_c), planar column-major, same operand order as
+// A_n = -i dt (H_s + sum_c a_c h_c), interleaved complex, column-major, same operand order as
 // linear_combine (src/sparse.py:325-334) and scaled (src/sparse.py:226-227).
 extern "C" __global__ void lg_k_dense_form(const double2* hs, const double2* const* hc, const double* amps, int Kc,
-                                           double dt, long count, double* Ar, double* Ai) {
+                                           double dt, long count, double2* A) {
   for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (long)gridDim.x * blockDim.x) {
     double hr = 0.0 + hs[q].x, hi = 0.0 + hs[q].y;
     for (int c = 0; c < Kc; ++c) {
@@ -251,8 +239,7 @@ extern "C" __global__ void lg_k_dense_form(const double2* hs, const double2* con
       hr = __dadd_rn(hr, __dmul_rn(v.x, a));
       hi = __dadd_rn(hi, __dmul_rn(v.y, a));
     }
-    Ar[q] = __dmul_rn(dt, hi);
-    Ai[q] = -__dmul_rn(dt, hr);
+    A[q] = make_double2(__dmul_rn(dt, hi), -__dmul_rn(dt, hr));
   }
 }
 

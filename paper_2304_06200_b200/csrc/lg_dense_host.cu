@@ -4,17 +4,16 @@
 
 namespace lgi {
 
-int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2* X, const double* Br,
-               const double* Bi, const double2* Xb, int C, double r, bool first, bool last, const double2* xin,
-               double2* cur, double2* tout) {
+int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2* B, const double2* Xb, int C,
+               double r, bool first, bool last, const double2* xin, double2* cur, double2* tout) {
   LgGemmArgs G{};
   const int d = (int)p->d;
   G.M = d;
   G.C = C;
-  G.seg[0] = LgGemmSeg{Ar, Ai, d, X, d, d};
+  G.seg[0] = LgGemmSeg{A, d, X, d, d};
   G.nseg = 1;
-  if (Br) {
-    G.seg[1] = LgGemmSeg{Br, Bi, d, Xb, d, d};
+  if (B) {
+    G.seg[1] = LgGemmSeg{B, d, Xb, d, d};
     G.nseg = 2;
   }
   G.xin = xin;
@@ -69,8 +68,8 @@ int dense_chain(lg_problem* p, int C, double sgn, int m, int s, const double2* x
   for (int si = 0; si < s; ++si)
     for (int j = 1; j <= m; ++j) {
       const bool first = si == 0 && j == 1;
-      int rc = dense_gemm(p, p->d_Ar, p->d_Ai, prev, nullptr, nullptr, nullptr, C, sgn * (1.0 / (double)(s * j)),
-                          first, j == m, first ? x : nullptr, cur, bufs[b]);
+      int rc = dense_gemm(p, p->d_Ad, prev, nullptr, nullptr, C, sgn * (1.0 / (double)(s * j)), first, j == m,
+                          first ? x : nullptr, cur, bufs[b]);
       if (rc) return rc;
       prev = bufs[b];
       b ^= 1;
@@ -93,15 +92,15 @@ int dense_aux_chain(lg_problem* p, int T, const int* gch, int G, int m, int s, c
         const int k = gch[gi];
         int rc;
         if (first)
-          rc = dense_gemm(p, p->d_Acr[k], p->d_Aci[k], psi, nullptr, nullptr, nullptr, T, r, true, last, nullptr,
-                          p->dd_xcur + gi * T * d, out + gi * T * d);
+          rc = dense_gemm(p, p->d_Acd[k], psi, nullptr, nullptr, T, r, true, last, nullptr, p->dd_xcur + gi * T * d,
+                          out + gi * T * d);
         else
-          rc = dense_gemm(p, p->d_Ar, p->d_Ai, prev + gi * T * d, p->d_Acr[k], p->d_Aci[k], prev + (long)G * T * d, T,
-                          r, false, last, nullptr, p->dd_xcur + gi * T * d, out + gi * T * d);
+          rc = dense_gemm(p, p->d_Ad, prev + gi * T * d, p->d_Acd[k], prev + (long)G * T * d, T, r, false, last,
+                          nullptr, p->dd_xcur + gi * T * d, out + gi * T * d);
         if (rc) return rc;
       }
-      int rc = dense_gemm(p, p->d_Ar, p->d_Ai, first ? psi : prev + (long)G * T * d, nullptr, nullptr, nullptr, T, r,
-                          first, last, first ? psi : nullptr, p->dd_xcur + (long)G * T * d, out + (long)G * T * d);
+      int rc = dense_gemm(p, p->d_Ad, first ? psi : prev + (long)G * T * d, nullptr, nullptr, T, r, first, last,
+                          first ? psi : nullptr, p->dd_xcur + (long)G * T * d, out + (long)G * T * d);
       if (rc) return rc;
       prev = out;
       b ^= 1;
@@ -109,10 +108,9 @@ int dense_aux_chain(lg_problem* p, int T, const int* gch, int G, int m, int s, c
   return LG_OK;
 }
 
-int dense_form(lg_problem* p, const double2* hs, double2** hc_dev, const double* amps, int kc, double dt, double* Ar,
-               double* Ai) {
+int dense_form(lg_problem* p, const double2* hs, double2** hc_dev, const double* amps, int kc, double dt, double2* A) {
   long count = p->d * p->d;
-  void* args[] = {&hs, &hc_dev, &amps, &kc, &dt, &count, &Ar, &Ai};
+  void* args[] = {&hs, &hc_dev, &amps, &kc, &dt, &count, &A};
   return launch(lg_dense_form_kernel(), dim3(148 * 8), dim3(256), args, 0, p->stream);
 }
 
@@ -192,14 +190,9 @@ int configure_dense(lg_problem* p) {
   }
   const long cst = (long)Tmax * (1 + Imax), cx = (long)(p->Kc + 1) * Tmax;
   DevMem& M = p->mem;
-  p->d_Ar = M.alloc<double>((size_t)d * d);
-  p->d_Ai = M.alloc<double>((size_t)d * d);
-  p->d_Acr.assign(p->Kc, nullptr);
-  p->d_Aci.assign(p->Kc, nullptr);
-  for (int c = 0; c < p->Kc; ++c) {
-    p->d_Acr[c] = M.alloc<double>((size_t)d * d);
-    p->d_Aci[c] = M.alloc<double>((size_t)d * d);
-  }
+  p->d_Ad = M.alloc<double2>((size_t)d * d);
+  p->d_Acd.assign(p->Kc, nullptr);
+  for (int c = 0; c < p->Kc; ++c) p->d_Acd[c] = M.alloc<double2>((size_t)d * d);
   p->dd_st = M.alloc<double2>((size_t)cst * d);
   p->dd_nx = M.alloc<double2>((size_t)cst * d);
   p->dd_cur = M.alloc<double2>((size_t)cst * d);
@@ -232,7 +225,7 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
   if (!(p->dense_dt == dt)) {
     for (int c = 0; c < Kc; ++c) {
       double2** none = nullptr;
-      rc = dense_form(p, p->d_hc_dense_host[c], none, nullptr, 0, dt, p->d_Acr[c], p->d_Aci[c]);
+      rc = dense_form(p, p->d_hc_dense_host[c], none, nullptr, 0, dt, p->d_Acd[c]);
       if (rc) return rc;
     }
     p->dense_dt = dt;
@@ -274,7 +267,7 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
     // ---- forward sweep
     for (long n = 0; n < N; ++n) {
       const int4 q = pl[(size_t)n * (Kc + 1)];
-      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ar, p->d_Ai);
+      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
       if (rc) return rc;
       rc = dense_chain(p, T, 1.0, q.x, q.y, p->dd_st, p->dd_cur);
       if (rc) return rc;
@@ -377,7 +370,7 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
     int gch[LG_MAX_CHANNELS];
     for (long n = N - 1; n >= 0; --n) {
       const int4* pn = &pl[(size_t)n * (Kc + 1)];
-      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ar, p->d_Ai);
+      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
       if (rc) return rc;
       const int cadj = n > 0 ? T * (1 + I) : T;
       rc = dense_chain(p, cadj, -1.0, pn[0].x, pn[0].y, p->dd_st, p->dd_nx);

@@ -143,8 +143,8 @@ struct lg_problem {
   int engine = 0;  // 0 legacy single-CTA, 1 legacy multi-CTA (grid barrier), 2 cta engine, 3 dense GEMM
   bool dense_large = false;
   // dense GEMM engine buffers
-  double *d_Ar = nullptr, *d_Ai = nullptr;
-  std::vector<double*> d_Acr, d_Aci;
+  double2* d_Ad = nullptr;           // dense engine: A_n = -i dt H_n, interleaved, column-major
+  std::vector<double2*> d_Acd;       // A_c = -i dt h_c per channel
   double2 *dd_st = nullptr, *dd_nx = nullptr, *dd_cur = nullptr, *dd_tb0 = nullptr, *dd_tb1 = nullptr,
           *dd_xcur = nullptr, *dd_xtb0 = nullptr, *dd_xtb1 = nullptr, *dd_tmp = nullptr;
   double2* dd_dots = nullptr;
@@ -276,8 +276,7 @@ void cl_color_slots(long d, int W, int R, const std::vector<int>& perm, const st
 // lg_dense_host.cu: dense (DMMA) engine driver
 int configure_dense(lg_problem* p);
 int run_dense(lg_problem* p, long N, double dt, bool grad);
-int dense_gemm(lg_problem* p, const double* Ar, const double* Ai, const double2* X, const double* Br,
-               const double* Bi, const double2* Xb, int C, double r, bool first, bool last, const double2* xin,
-               double2* cur, double2* tout);
+int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2* B, const double2* Xb, int C,
+               double r, bool first, bool last, const double2* xin, double2* cur, double2* tout);
 
 }  // namespace lgi

@@ -136,8 +136,7 @@ struct LgFinalArgs {
 
 // ---- host <-> dense-path kernel arguments (lg_dense.cu; filled by the host units)
 struct LgGemmSeg {
-  const double* Ar;
-  const double* Ai;
+  const double2* A;  // interleaved complex, column-major
   int lda;
   const double2* X;
   int ldx;
