@@ -363,7 +363,9 @@ const char* lg_engine_name(lg_problem* p) {
     case 2: return "cta:lg_k_cta_backward";
     case 3: return "dense:lg_k_zgemm_taylor";
     case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
-    case 5: return p->cl_split ? "cluster-split:lg_k_cl_backward" : "cluster:lg_k_cl_backward";
+    case 5:
+      return p->cl_split ? "cluster-split:lg_k_cl_backward"
+                         : (p->cl_small >= 3 ? "cluster-large:lg_k_cll_backward" : "cluster:lg_k_cl_backward");
     default: return "unknown";
   }
 }

@@ -253,6 +253,48 @@ bool configure_cl(lg_problem* p, int smem_optin) {
     if (ncl >= (int)gset.size()) break;
   }
   if (Q == 0) return false;
+  // LARGE kernels (lg_sweep_cl_large.cuh): more rows per CTA than the SMALL kernels take, one term per
+  // exchange, control width <= 2 -- two rows per thread at 320 threads (168-register budget).  Measured
+  // on c4 (N' = 400): forward 114.8 -> 94.5 ms, backward 795.7 -> 781.6 ms against the generic kernels;
+  // three rows per thread at 224 threads (255 registers, 7 warps): 108.8 / 795.3 ms.
+  int threads = 32 * ((R + 2 * E + 31) / 32);
+  const bool force_large = std::getenv("LG_CL_LARGE") && std::atoi(std::getenv("LG_CL_LARGE")) == 1;
+  const int rpt = 2, LT = 320, lsm = 3;
+  if ((!small || force_large) && Q == 1 && p->Wc <= 2 && R <= rpt * LT && !std::getenv("LG_CL_NOLARGE")) {
+    const int cstl = cmax | 1;
+    const int wf = lg_cll_mb_word(R, H, LT, cstl, 0, rpt) + 1, wbl = lg_cll_mb_word(R, H, LT, cstl, p->Kc * 2, rpt) + 1;
+    void* ff = lg_cl_kernel(0, p->W, maxc, lsm);
+    void* fb = lg_cl_kernel(1, p->W, maxc, lsm);
+    int ncl = 0;
+    if (ff && fb && (long)wbl * 16 <= cap && 16L * cstl * (R + 2 * H) < 65536 &&
+        cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, wf * 16) == cudaSuccess &&
+        cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, wbl * 16) == cudaSuccess &&
+        (CS <= 8 || (cudaFuncSetAttribute(ff, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                     cudaFuncSetAttribute(fb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess))) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(LT);
+      cfg.dynamicSmemBytes = wbl * 16;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&ncl, fb, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        ncl = 0;
+      }
+    }
+    if (ncl >= 1 && (force_large || ncl >= std::min(best_ncl, (int)gset.size()))) {
+      small = lsm;
+      words = wf;
+      words_b = wbl;
+      acs = true;
+      threads = LT;
+    }
+  }
   if (cudaFuncSetAttribute(lg_cl_kernel(0, p->W, maxc, small), cudaFuncAttributeMaxDynamicSharedMemorySize, words * 16) !=
           cudaSuccess ||
       cudaFuncSetAttribute(lg_cl_kernel(1, p->W, maxc, small), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -295,13 +337,13 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_smem_b = words_b * 16;
   p->cl_acs = acs ? 1 : 0;
   p->cta_Imax = Imax;
-  p->threads = 32 * ((R + 2 * E + 31) / 32);
+  p->threads = threads;
   // Split backward (lg_k_cl_backward<..., SPLIT>): the cluster's two halves run the adjoint
   // chain and the aux chains of consecutive steps concurrently over a row partition of
   // R_b = d / (CS / 2) rows.  Taken when the SMALL kernel fits (<= 192 threads, two CTAs per
   // SM) and every trajectory's cluster stays resident.
   p->cl_split = 0;
-  if (small && CS == 16 && p->Kc >= 1 && !(std::getenv("LG_CL_SPLIT") && std::atoi(std::getenv("LG_CL_SPLIT")) == 0)) {
+  if (small == 1 && CS == 16 && p->Kc >= 1 && !(std::getenv("LG_CL_SPLIT") && std::atoi(std::getenv("LG_CL_SPLIT")) == 0)) {
     const int rb = (int)((d + 7) / 8);
     int qb = rb <= 200 ? std::max(1, std::min(6, 1 + ((H + 7) / 8 * 8) / H)) : 1;
     while (qb > 1 && (ext(qb) + H > rb)) --qb;

@@ -264,7 +264,18 @@ extern "C" __global__ void lg_k_dots(const __grid_constant__ LgDotArgs D) {
   if (threadIdx.x == 0) {
     double2 s = make_double2(0.0, 0.0);
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s.x += red[w].x, s.y += red[w].y;
-    *D.out[p] = s;
+    // per-step scalars accumulate on the device in step order (the launches are stream-ordered)
+    if (D.mode[p] == 0) {
+      *D.out[p] = s;
+    } else {
+      double* acc = reinterpret_cast<double*>(D.out[p]);
+      if (D.mode[p] == 1) {
+        *acc += s.x;
+      } else {
+        const double h = hypot(s.x, s.y);
+        *acc += h * h;
+      }
+    }
   }
 }
 

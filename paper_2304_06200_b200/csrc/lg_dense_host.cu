@@ -114,9 +114,14 @@ int dense_form(lg_problem* p, const double2* hs, double2** hc_dev, const double*
   return launch(lg_dense_form_kernel(), dim3(148 * 8), dim3(256), args, 0, p->stream);
 }
 
-// deterministic dots over pairs; results copied to host
-int dense_dots(lg_problem* p, const std::vector<std::pair<const double2*, const double2*>>& pr, std::vector<double2>& out) {
-  out.assign(pr.size(), make_double2(0.0, 0.0));
+// deterministic dots over pairs, written (mode 0) or accumulated (modes 1, 2: running costs, in step
+// order) straight into the device-side raw scalars: no host round trip inside the sweeps
+struct DotOut {
+  double2* out;
+  int mode;
+};
+int dense_dots(lg_problem* p, const std::vector<std::pair<const double2*, const double2*>>& pr,
+               const std::vector<DotOut>& to) {
   for (size_t b0 = 0; b0 < pr.size(); b0 += 64) {
     LgDotArgs D{};
     D.d = (int)p->d;
@@ -124,15 +129,12 @@ int dense_dots(lg_problem* p, const std::vector<std::pair<const double2*, const 
     for (int q = 0; q < D.n; ++q) {
       D.u[q] = pr[b0 + q].first;
       D.v[q] = pr[b0 + q].second;
-      D.out[q] = p->dd_dots + b0 + q;
+      D.out[q] = to[b0 + q].out;
+      D.mode[q] = to[b0 + q].mode;
     }
     void* args[] = {&D};
     int rc = launch(lg_dots_kernel(), dim3(D.n), dim3(256), args, 0, p->stream);
     if (rc) return rc;
-  }
-  if (!pr.empty()) {
-    CK(cudaMemcpyAsync(out.data(), p->dd_dots, sizeof(double2) * pr.size(), cudaMemcpyDeviceToHost, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
   }
   return LG_OK;
 }
@@ -158,8 +160,9 @@ int dense_ell(lg_problem* p, const Spec& sp, const std::vector<const double2*>& 
   return LG_OK;
 }
 
+// y_q (+)= alpha_q u_q; alpha_q from the device (alpha_ptr[q]) when given, else the host value
 int dense_axpy(lg_problem* p, const std::vector<const double2*>& u, const std::vector<double2*>& y,
-               const std::vector<double2>& alpha, bool acc) {
+               const std::vector<double2>& alpha, const std::vector<const double2*>& alpha_ptr, bool acc) {
   for (size_t b0 = 0; b0 < u.size(); b0 += 64) {
     LgAxpyArgs A{};
     A.d = (int)p->d;
@@ -168,7 +171,7 @@ int dense_axpy(lg_problem* p, const std::vector<const double2*>& u, const std::v
       A.u[q] = u[b0 + q];
       A.y[q] = y[b0 + q];
       A.alpha[q] = alpha[b0 + q];
-      A.alpha_ptr[q] = nullptr;
+      A.alpha_ptr[q] = alpha_ptr[b0 + q];
       A.accumulate[q] = acc;
     }
     void* args[] = {&A};
@@ -213,14 +216,16 @@ int configure_dense(lg_problem* p) {
   return LG_OK;
 }
 
+// One evaluation on the dense engine.  The host drives the per-step GEMM chains (the Taylor
+// plans are read back once, before the sweeps); every per-step scalar -- overlaps, running
+// costs, traces, <lambda|dU/da psi> -- is produced and accumulated on the device, in the raw
+// layout the finalize kernel and the sharded all-reduce hook read (lg_raw_get).
 int run_dense(lg_problem* p, long N, double dt, bool grad) {
   const long d = p->d;
   const int Kc = p->Kc, S = (int)p->specs.size(), Tt = p->T_total;
   int rc;
   std::vector<int4> pl((size_t)N * (Kc + 1));
   CK(cudaMemcpyAsync(pl.data(), p->d_plan, sizeof(int4) * pl.size(), cudaMemcpyDeviceToHost, p->stream));
-  std::vector<double> amps((size_t)N * Kc);
-  CK(cudaMemcpyAsync(amps.data(), p->d_amps, sizeof(double) * amps.size(), cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (!(p->dense_dt == dt)) {
     for (int c = 0; c < Kc; ++c) {
@@ -230,22 +235,20 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
     }
     p->dense_dt = dt;
   }
-  std::vector<double2> ip((size_t)N * std::max(S, 1) * Kc * std::max(Tt, 1), make_double2(0, 0)),
-      fin((size_t)std::max(S, 1) * std::max(Tt, 1), make_double2(0, 0)),
-      trp((size_t)std::max(S, 1) * N * std::max(Tt, 1), make_double2(0, 0));
-  std::vector<double> run((size_t)std::max(S, 1) * std::max(Tt, 1), 0.0);
-  std::vector<double2> dots;
-  // sharded running gate costs: every rank all-reduces the set's traces between its sweeps
+  const size_t Sx = std::max(S, 1), Tx = std::max(Tt, 1);
+  CK(cudaMemsetAsync(p->d_run, 0, sizeof(double) * Sx * Tx, p->stream));
+  CK(cudaMemsetAsync(p->d_fin, 0, sizeof(double2) * Sx * Tx, p->stream));
+  if (grad) CK(cudaMemsetAsync(p->d_ip, 0, sizeof(double2) * N * Sx * Kc * Tx, p->stream));
+  CK(cudaMemsetAsync(p->d_trp, 0, sizeof(double2) * Sx * N * Tx, p->stream));
+  auto runp = [&](long o) { return reinterpret_cast<double2*>(p->d_run + o); };
+  // sharded running gate costs: every rank all-reduces the traces between its sweeps
   auto trace_hook = [&](int set) -> int {
     if (!grad || !p->hook) return LG_OK;
     bool any = false;
     for (int s = 0; s < S; ++s) any |= p->specs[s].set == set && p->specs[s].kind == LGK_GATE_RUN;
     if (!any) return LG_OK;
-    CK(cudaMemcpyAsync(p->d_trp, trp.data(), sizeof(double2) * trp.size(), cudaMemcpyHostToDevice, p->stream));
-    if (p->hook(reinterpret_cast<double*>(p->d_trp), 2 * (long)trp.size(), p->stream, p->hook_user) != 0)
+    if (p->hook(reinterpret_cast<double*>(p->d_trp), 2 * (long)Sx * N * Tx, p->stream, p->hook_user) != 0)
       return fail(LG_CUDA_ERROR, "all-reduce hook failed (traces)");
-    CK(cudaMemcpyAsync(trp.data(), p->d_trp, sizeof(double2) * trp.size(), cudaMemcpyDeviceToHost, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
     p->trp_reduced = true;
     return LG_OK;
   };
@@ -274,97 +277,95 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
       CK(cudaMemcpyAsync(p->dd_st, p->dd_cur, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
       const bool fin_step = n == N - 1;
       std::vector<std::pair<const double2*, const double2*>> pr;
-      std::vector<std::pair<int, int>> who;  // (spec, t)
+      std::vector<DotOut> to;
       for (int s : sp_idx) {
         const int kind = p->specs[s].kind;
+        for (int t = 0; t < T; ++t) {
+          const long o = (long)s * Tt + t0 + t;
+          if (kind == LGK_STATE_PEN) {
+            pr.push_back({col(p->dd_st, t), col(p->dd_tmp, t)});
+            to.push_back({runp(o), 1});
+          } else if (kind == LGK_STATE_RUN) {
+            pr.push_back({tgt(s, t), col(p->dd_st, t)});
+            to.push_back({runp(o), 2});
+          } else if (kind == LGK_GATE_RUN) {
+            pr.push_back({tgt(s, t), col(p->dd_st, t)});
+            to.push_back({p->d_trp + ((long)s * N + n) * Tt + t0 + t, 0});
+          } else if (fin_step && kind == LGK_GATE) {
+            pr.push_back({tgt(s, t), col(p->dd_st, t)});
+            to.push_back({p->d_fin + o, 0});
+          } else if (fin_step && kind == LGK_STATE_INF) {
+            pr.push_back({col(p->dd_st, t), tgt(s, t)});
+            to.push_back({p->d_fin + o, 0});
+          }
+        }
         if (kind == LGK_STATE_PEN) {
+          // Omega psi_n into tmp, and the penalty dots taken before tmp is reused by another penalty term
           std::vector<const double2*> x;
           std::vector<double2*> y;
           for (int t = 0; t < T; ++t) x.push_back(col(p->dd_st, t)), y.push_back(col(p->dd_tmp, t));
           rc = dense_ell(p, p->specs[s], x, y, false);
           if (rc) return rc;
-          for (int t = 0; t < T; ++t) pr.push_back({col(p->dd_st, t), col(p->dd_tmp, t)}), who.push_back({s, t});
-        } else if (kind == LGK_STATE_RUN || kind == LGK_GATE_RUN || (fin_step && kind == LGK_GATE)) {
-          for (int t = 0; t < T; ++t) pr.push_back({tgt(s, t), col(p->dd_st, t)}), who.push_back({s, t});
-        } else if (fin_step && kind == LGK_STATE_INF) {
-          for (int t = 0; t < T; ++t) pr.push_back({col(p->dd_st, t), tgt(s, t)}), who.push_back({s, t});
-        }
-        if (kind == LGK_STATE_PEN && !pr.empty()) {
-          // penalty dots must be taken before tmp is reused by another penalty term
-          rc = dense_dots(p, pr, dots);
+          rc = dense_dots(p, pr, to);
           if (rc) return rc;
-          for (size_t z = 0; z < pr.size(); ++z) {
-            const int s2 = who[z].first, t = who[z].second;
-            const long o = (long)s2 * Tt + t0 + t;
-            const int k2 = p->specs[s2].kind;
-            if (k2 == LGK_STATE_PEN) run[o] += dots[z].x;
-            else if (k2 == LGK_STATE_RUN) { const double a = std::hypot(dots[z].x, dots[z].y); run[o] += a * a; }
-            else if (k2 == LGK_GATE_RUN) trp[((long)s2 * N + n) * Tt + t0 + t] = dots[z];
-            else fin[o] = dots[z];
-          }
           pr.clear();
-          who.clear();
+          to.clear();
         }
       }
-      rc = dense_dots(p, pr, dots);
+      rc = dense_dots(p, pr, to);
       if (rc) return rc;
-      for (size_t z = 0; z < pr.size(); ++z) {
-        const int s2 = who[z].first, t = who[z].second;
-        const long o = (long)s2 * Tt + t0 + t;
-        const int k2 = p->specs[s2].kind;
-        if (k2 == LGK_STATE_PEN) run[o] += dots[z].x;
-        else if (k2 == LGK_STATE_RUN) { const double a = std::hypot(dots[z].x, dots[z].y); run[o] += a * a; }
-        else if (k2 == LGK_GATE_RUN) trp[((long)s2 * N + n) * Tt + t0 + t] = dots[z];
-        else fin[o] = dots[z];
-      }
     }
     CK(cudaMemcpyAsync(p->d_psiN + (long)t0 * d, p->dd_st, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
     if (int rh = trace_hook(set)) return rh;
     if (!grad || I == 0) continue;
-    // running gate traces summed over the set (trajectory order)
-    std::vector<double2> trsum((size_t)S * N, make_double2(0, 0));
-    for (int s : sp_idx)
-      if (p->specs[s].kind == LGK_GATE_RUN)
-        for (long n = 0; n < N; ++n)
-          for (int t = 0; t < p->set_T[set]; ++t) {
-            const double2 v = trp[((long)s * N + n) * Tt + p->set_t0[set] + t];
-            trsum[(size_t)s * N + n].x += v.x;
-            trsum[(size_t)s * N + n].y += v.y;
-          }
+    bool gate_run = false;
+    for (int s : sp_idx) gate_run |= p->specs[s].kind == LGK_GATE_RUN;
+    if (gate_run) {  // running gate traces summed over the set (trajectory order), on the device
+      int Ni = (int)N, Sv = S, Tv = Tt;
+      long cnt = (long)S * N;
+      void* targs[] = {&p->d_trp, &Sv, &Ni, &Tv, &p->d_spec_t0, &p->d_spec_K, &p->d_trsum};
+      rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
+      if (rc) return rc;
+    }
     auto lam = [&](double2* base, int si, int t) { return col(base, T + si * T + t); };
-    // ---- costate initialisation (src/costs.py:312-321, :457-460)
-    {
+    // overlaps <phi|psi> of the running state costs: device scratch read by the axpy kernel
+    auto run_overlaps = [&](double2* psi_base) -> int {
       std::vector<std::pair<const double2*, const double2*>> pr;
+      std::vector<DotOut> to;
       for (int si = 0; si < I; ++si)
         if (p->specs[sp_idx[si]].kind == LGK_STATE_RUN)
-          for (int t = 0; t < T; ++t) pr.push_back({tgt(sp_idx[si], t), col(p->dd_st, t)});
-      rc = dense_dots(p, pr, dots);
-      if (rc) return rc;
-      size_t z = 0;
-      for (int si = 0; si < I; ++si) {
-        const int s = sp_idx[si];
-        const Spec& sp = p->specs[s];
-        std::vector<const double2*> u;
+          for (int t = 0; t < T; ++t) {
+            pr.push_back({tgt(sp_idx[si], t), col(psi_base, t)});
+            to.push_back({p->dd_dots + si * T + t, 0});
+          }
+      return dense_dots(p, pr, to);
+    };
+    // ---- costate initialisation (src/costs.py:312-321, :457-460)
+    rc = run_overlaps(p->dd_st);
+    if (rc) return rc;
+    for (int si = 0; si < I; ++si) {
+      const int s = sp_idx[si];
+      const Spec& sp = p->specs[s];
+      if (sp.kind == LGK_STATE_PEN) {
+        std::vector<const double2*> x;
+        std::vector<double2*> yy;
+        for (int t = 0; t < T; ++t) x.push_back(col(p->dd_st, t)), yy.push_back(lam(p->dd_st, si, t));
+        rc = dense_ell(p, sp, x, yy, false);
+      } else {
+        std::vector<const double2*> u, ap;
         std::vector<double2*> y;
         std::vector<double2> al;
         for (int t = 0; t < T; ++t) {
-          if (sp.kind == LGK_STATE_PEN) continue;
           u.push_back(tgt(s, t));
           y.push_back(lam(p->dd_st, si, t));
-          if (sp.kind == LGK_STATE_RUN) al.push_back(dots[z++]);
-          else if (sp.kind == LGK_GATE_RUN) al.push_back(trsum[(size_t)s * N + N - 1]);
-          else al.push_back(make_double2(1.0, 0.0));
+          al.push_back(make_double2(1.0, 0.0));
+          ap.push_back(sp.kind == LGK_STATE_RUN   ? p->dd_dots + si * T + t
+                       : sp.kind == LGK_GATE_RUN ? p->d_trsum + (long)s * N + N - 1
+                                                 : nullptr);
         }
-        if (sp.kind == LGK_STATE_PEN) {
-          std::vector<const double2*> x;
-          std::vector<double2*> yy;
-          for (int t = 0; t < T; ++t) x.push_back(col(p->dd_st, t)), yy.push_back(lam(p->dd_st, si, t));
-          rc = dense_ell(p, sp, x, yy, false);
-        } else {
-          rc = dense_axpy(p, u, y, al, false);
-        }
-        if (rc) return rc;
+        rc = dense_axpy(p, u, y, al, ap, false);
       }
+      if (rc) return rc;
     }
     // ---- backward sweep
     int gch[LG_MAX_CHANNELS];
@@ -386,27 +387,22 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
           }
         rc = dense_aux_chain(p, T, gch, G, pn[1 + kc].x, pn[1 + kc].y, p->dd_nx);
         if (rc) return rc;
+        // <lambda_s(n)| dU_n/da_k psi_{n-1}> straight into ip (src/costs.py:328-339)
         std::vector<std::pair<const double2*, const double2*>> pr;
+        std::vector<DotOut> to;
         for (int gi = 0; gi < G; ++gi)
           for (int si = 0; si < I; ++si)
-            for (int t = 0; t < T; ++t) pr.push_back({lam(p->dd_st, si, t), p->dd_xcur + ((long)gi * T + t) * d});
-        rc = dense_dots(p, pr, dots);
+            for (int t = 0; t < T; ++t) {
+              pr.push_back({lam(p->dd_st, si, t), p->dd_xcur + ((long)gi * T + t) * d});
+              to.push_back({p->d_ip + (((long)n * S + sp_idx[si]) * Kc + gch[gi]) * Tt + t0 + t, 0});
+            }
+        rc = dense_dots(p, pr, to);
         if (rc) return rc;
-        size_t z = 0;
-        for (int gi = 0; gi < G; ++gi)
-          for (int si = 0; si < I; ++si)
-            for (int t = 0; t < T; ++t)
-              ip[(((size_t)n * S + sp_idx[si]) * Kc + gch[gi]) * Tt + t0 + t] = dots[z++];
       }
       if (n == 0) break;
       // costate sources at psi_{n-1} (src/costs.py:341-353, :474-479)
-      std::vector<std::pair<const double2*, const double2*>> pr;
-      for (int si = 0; si < I; ++si)
-        if (p->specs[sp_idx[si]].kind == LGK_STATE_RUN)
-          for (int t = 0; t < T; ++t) pr.push_back({tgt(sp_idx[si], t), col(p->dd_nx, t)});
-      rc = dense_dots(p, pr, dots);
+      rc = run_overlaps(p->dd_nx);
       if (rc) return rc;
-      size_t z = 0;
       for (int si = 0; si < I; ++si) {
         const int s = sp_idx[si];
         const Spec& sp = p->specs[s];
@@ -416,15 +412,16 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
           for (int t = 0; t < T; ++t) x.push_back(col(p->dd_nx, t)), yy.push_back(lam(p->dd_nx, si, t));
           rc = dense_ell(p, sp, x, yy, true);
         } else if (sp.kind == LGK_STATE_RUN || sp.kind == LGK_GATE_RUN) {
-          std::vector<const double2*> u;
+          std::vector<const double2*> u, ap;
           std::vector<double2*> y;
           std::vector<double2> al;
           for (int t = 0; t < T; ++t) {
             u.push_back(tgt(s, t));
             y.push_back(lam(p->dd_nx, si, t));
-            al.push_back(sp.kind == LGK_STATE_RUN ? dots[z++] : trsum[(size_t)s * N + n - 1]);
+            al.push_back(make_double2(0.0, 0.0));
+            ap.push_back(sp.kind == LGK_STATE_RUN ? p->dd_dots + si * T + t : p->d_trsum + (long)s * N + n - 1);
           }
-          rc = dense_axpy(p, u, y, al, true);
+          rc = dense_axpy(p, u, y, al, ap, true);
         } else {
           rc = LG_OK;
         }
@@ -433,11 +430,6 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
       CK(cudaMemcpyAsync(p->dd_st, p->dd_nx, sizeof(double2) * T * (1 + I) * d, cudaMemcpyDeviceToDevice, p->stream));
     }
   }
-  CK(cudaMemcpyAsync(p->d_ip, ip.data(), sizeof(double2) * ip.size(), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaMemcpyAsync(p->d_fin, fin.data(), sizeof(double2) * fin.size(), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaMemcpyAsync(p->d_trp, trp.data(), sizeof(double2) * trp.size(), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaMemcpyAsync(p->d_run, run.data(), sizeof(double) * run.size(), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaStreamSynchronize(p->stream));
   return LG_OK;
 }
 

@@ -370,6 +370,7 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.diag_Ud = p->d_Ud;
   E.diag_D = p->d_D;
   E.cl_acs = 0;
+  E.dbg = std::getenv("LG_DBG") ? std::atoi(std::getenv("LG_DBG")) : 0;
   E.ws_nw = p->ws_nw;
   E.dense_rows = (p->dense && p->W == p->d && p->Wc == p->d) ? 1 : 0;
   E.cl_perm = p->d_cl_perm;

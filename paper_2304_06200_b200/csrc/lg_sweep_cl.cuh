@@ -34,11 +34,17 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cdot(double2 a, double2 b) {
   return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
-__device__ __forceinline__ void cmac(double2& p, double2& q, double2 a, double2 x) {
+// p += a x with the a.y terms in q (four independent chains), or all in p when split is false
+__device__ __forceinline__ void cmac(double2& p, double2& q, double2 a, double2 x, bool split = true) {
   p.x = fma(a.x, x.x, p.x);
   p.y = fma(a.x, x.y, p.y);
-  q.x = fma(-a.y, x.y, q.x);
-  q.y = fma(a.y, x.x, q.y);
+  if (split) {
+    q.x = fma(-a.y, x.y, q.x);
+    q.y = fma(a.y, x.x, q.y);
+  } else {
+    p.x = fma(-a.y, x.y, p.x);
+    p.y = fma(a.y, x.x, p.y);
+  }
 }
 __device__ __forceinline__ double2 warp_sum(double2 v) {
   for (int o = 16; o > 0; o >>= 1) {
@@ -828,6 +834,8 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
   cl_sync();
 }
 
+#include "lg_sweep_cl_large.cuh"
+
 // Instantiations for one ELL width per translation unit (lg_sweep_cl_w*.cu), so the
 // build compiles them in parallel.
 #define LG_CL_KERNELS(W_)                                                                              \
@@ -843,4 +851,5 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
     return backward ? (void*)lg_k_cl_backward<W_, C_, false> : (void*)lg_k_cl_forward<W_, C_, false>;        \
   case C_ * 2 + 1:                                                                                           \
     if (small == 2) return backward ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;                 \
+    if (small == 3) return backward ? (void*)lg_k_cll_backward<W_, C_, 2> : (void*)lg_k_cll_forward<W_, C_, 2>;\
     return backward ? (void*)lg_k_cl_backward<W_, C_, true> : (void*)lg_k_cl_forward<W_, C_, true>;

@@ -17,6 +17,14 @@ __host__ __device__ inline int lg_cl_mb_word(int R, int H, int Q, int E, int cma
          (acw * T + 3) / 4;
 }
 
+// LARGE cluster kernels (lg_sweep_cl_large.cuh): two rows per thread (T threads, R <= 2 T),
+// one Taylor term per exchange.  Reduction scratch, 1/(s j) table, two window buffers of cmax
+// columns, staged control rows [acw][2 T] (values, then int columns), then the two exchange
+// mbarriers (one 16-byte word).
+__host__ __device__ inline int lg_cll_mb_word(int R, int H, int T, int cmax, int acw, int rpt) {
+  return 16 * 32 + 16 * 16 + 72 + 2 * cmax * (R + 2 * H) + acw * rpt * T + (acw * rpt * T + 3) / 4;
+}
+
 // Cost kinds (src/costs.py:49-61)
 enum LgKind { LGK_STATE_INF = 0, LGK_STATE_PEN = 1, LGK_STATE_RUN = 2, LGK_GATE = 3, LGK_GATE_RUN = 4 };
 
@@ -112,6 +120,7 @@ struct LgEngineArgs {
   const double2* diag_Ud;
   const double2* diag_D;
   int cl_acs;               // backward stages the control-generator rows in shared memory
+  int dbg;                  // LG_DBG bits (timing experiments only; results are wrong when set)
   int ws_nw;                // ws cluster backward: derivative workers per control channel
   int dense_rows;           // every operator row stores all d columns in order (dense H): slot w == column w
   const int* cl_perm;       // [d] renumbered row -> original row
@@ -162,6 +171,7 @@ struct LgDotArgs {
   const double2* u[64];
   const double2* v[64];
   double2* out[64];
+  int mode[64];  // 0: *out = <u|v>; 1: ((double*)out)[0] += Re<u|v>; 2: ((double*)out)[0] += |<u|v>|^2
 };
 struct LgEllArgs {
   int d, W, ncol, accumulate;

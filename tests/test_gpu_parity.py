@@ -232,14 +232,18 @@ def test_c5_prefix_dense_dmma():
 # ----------------------------------------------------------------------------- cluster-engine variants
 
 
-@pytest.mark.parametrize("size,q,nosmall", [(16, 1, 0), (16, 3, 0), (16, 6, 0), (8, 3, 0), (16, 3, 1), (8, 2, 1)])
+@pytest.mark.parametrize("size,q,nosmall", [(16, 1, 0), (16, 3, 0), (16, 6, 0), (8, 3, 0), (16, 3, 1), (8, 2, 1),
+                                            (16, 1, 2), (8, 1, 2)])
 def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
-    """Every cluster-engine layout (cluster size, ghost-zone block length Q, SMALL or generic
-    kernels) against the golden c3 prefix and the plan-sensitive block-aux stress variant."""
+    """Every cluster-engine layout (cluster size, ghost-zone block length Q, SMALL, generic or
+    LARGE (three rows per thread, nosmall == 2) kernels) against the golden c3 prefix and the
+    plan-sensitive block-aux stress variant."""
     monkeypatch.setenv("LG_CL_SIZE", str(size))
     monkeypatch.setenv("LG_CL_Q", str(q))
-    if nosmall:
+    if nosmall == 1:
         monkeypatch.setenv("LG_CL_NOSMALL", "1")
+    if nosmall == 2:
+        monkeypatch.setenv("LG_CL_LARGE", "1")
     z = G.load("c3")
     hs, hc = G.mats(z)
     prob = ControlProblem(hs, tuple(hc), initial_state=z["psi0"])
@@ -249,7 +253,7 @@ def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
     for _ in range(4):  # repeated gradient and forward-only calls on one problem (intermittent-race guard)
         _check(npb.grad(a), z["cost"], z["grad"])
         assert abs(npb.cost(a) - float(z["cost"])) <= COST_TOL
-    assert npb.engine.startswith("cluster"), npb.engine
+    assert npb.engine.startswith("cluster-large" if nosmall == 2 else "cluster"), npb.engine
     zs = G.sub(G.load("stress"), "s_block160")
     hs, hc = G.mats(zs)
     om = G.penalty(zs)
