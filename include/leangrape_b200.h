@@ -100,6 +100,12 @@ int lg_eval(lg_problem* p, int64_t n_steps, double dt, const double* amps, doubl
 /* composite_cost: forward sweeps only (line search, src/optimizer.py:153-170). */
 int lg_cost(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* cost);
 
+/* composite_cost of n_fields candidate fields in ONE forward launch (the line search's trial
+ * fields, src/optimizer.py:153-170): amps[c][n_steps][n_channels], costs[c].  Each cost is
+ * bit-identical to lg_cost on that field.  LG_UNSUPPORTED on engines without a batched forward
+ * kernel (dense GEMM, DIAGONALIZATION backend) and on sharded problems. */
+int lg_cost_batch(lg_problem* p, int32_t n_fields, int64_t n_steps, double dt, const double* amps, double* costs);
+
 /* Same as lg_eval, but with amplitudes already resident on the device and the
  * results left on the device (benchmarking the kernels without host copies). */
 int lg_eval_device(lg_problem* p, int64_t n_steps, double dt, const double* d_amps, double* d_cost, double* d_grad);

@@ -347,6 +347,16 @@ class NativeProblem:
         _native.check(self._lib.lg_cost(self.handle, a.n_steps, float(a.dt), _native.dptr(amps), C.byref(cost)))
         return float(cost.value)
 
+    def cost_batch(self, fields) -> list:
+        """Costs of several fields with the same (n_steps, dt) in one forward launch
+        (``lg_cost_batch``); NotImplementedError on engines without a batched forward kernel."""
+        amps = np.ascontiguousarray(np.stack([a.amplitudes for a in fields]), np.float64)
+        out = np.zeros(len(fields), np.float64)
+        a0 = fields[0]
+        _native.check(self._lib.lg_cost_batch(self.handle, len(fields), a0.n_steps, float(a0.dt), _native.dptr(amps),
+                                              _native.dptr(out)))
+        return [float(c) for c in out]
+
     def forward_states(self, a: ControlField, k: int) -> np.ndarray:
         amps = np.ascontiguousarray(a.amplitudes, np.float64)
         out = np.zeros((k, self.dim), np.complex128)
@@ -467,8 +477,11 @@ _POOLS: "OrderedDict[tuple, tuple]" = OrderedDict()
 
 def composite_cost_batch(problem: ControlProblem, fields, terms) -> list:
     """``composite_cost`` for several fields at once (the line-search path,
-    src/optimizer.py:153-170).  Each field gets its own device problem and stream and the
-    evaluations run concurrently; every cost is bit-identical to ``composite_cost`` of that field."""
+    src/optimizer.py:153-170).  Fields with a common (n_steps, dt) go through ``lg_cost_batch``:
+    one forward launch over (candidate, trajectory) for the warp-specialised and cluster engines.
+    Other engines (dense GEMM, DIAGONALIZATION) give each field its own device problem and stream
+    and run the evaluations concurrently.  Every cost is bit-identical to ``composite_cost`` of
+    that field."""
     from concurrent.futures import ThreadPoolExecutor
 
     terms, has_state = _split(terms)
@@ -479,6 +492,12 @@ def composite_cost_batch(problem: ControlProblem, fields, terms) -> list:
         raise ValueError("state-transfer terms require problem.initial_state")
     if not fields:
         return []
+    if len(fields) > 1 and len({(a.n_steps, float(a.dt)) for a in fields}) == 1:
+        npb = _native_for(problem, terms, problem.initial_state if has_state else None, problem.basis)
+        try:
+            return npb.cost_batch(fields)
+        except NotImplementedError:
+            pass
     key = (id(problem), tuple(id(t) for t in terms))
     hit = _POOLS.get(key)
     pool = list(hit[0]) if hit else []

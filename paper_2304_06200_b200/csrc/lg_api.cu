@@ -483,6 +483,105 @@ int lg_cost(lg_problem* p, int64_t n_steps, double dt, const double* amps, doubl
   return LG_OK;
 }
 
+// composite_cost for k candidate fields in one forward launch (src/optimizer.py:153-170: the
+// backtracking line search's trial fields): the k x N step generators and plans are prepared as
+// one batch of steps, and the forward kernel takes candidate c from blockIdx.y with its own
+// slice of generators, plans and raw outputs.  Costs are bit-identical to k lg_cost calls.
+int lg_cost_batch(lg_problem* p, int32_t n_fields, int64_t n_steps, double dt, const double* amps, double* costs) {
+  const long k = n_fields, N = n_steps;
+  if (!p) return fail(LG_INVALID_ARG, "null problem handle");
+  if (k < 1) return fail(LG_INVALID_ARG, "need at least one candidate field");
+  int rc = check_field(p, k * N, dt, amps);
+  if (rc) return rc;
+  if (p->specs.empty()) return fail(LG_INVALID_ARG, "composite cost needs at least one term");
+  if (p->backend == 1 || !(p->engine == 4 || p->engine == 5) || p->shard_e < (1L << 40) || p->n_groups < 1)
+    return fail(LG_UNSUPPORTED, "batched candidates need the warp-specialised or cluster engine on an unsharded problem");
+  if (k > 65535) return fail(LG_INVALID_ARG, "too many candidate fields");
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, k * N);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * k * N * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, k * N, dt, false);
+  if (rc) return rc;
+  const long S = std::max<long>((long)p->specs.size(), 1), T = std::max(p->T_total, 1);
+  const long runsz = (S * T + 1) / 2 * 2;  // keeps trp (complex) 16-byte aligned
+  const long per = 2 * S * T + runsz + 2 * S * N * T;  // doubles: fin (complex), run, trp (complex)
+  if (k > p->bcap_k || N > p->bcap_N) {
+    p->bmem.release();
+    p->bcap_k = p->bcap_N = 0;
+    p->d_bat = p->bmem.alloc<double>((size_t)k * per);
+    p->d_bpsi = p->bmem.alloc<double2>((size_t)k * T * p->d);
+    p->d_bcost = p->bmem.alloc<double>((size_t)k);
+    p->d_bEA = p->bmem.alloc<LgEngineArgs>((size_t)k);
+    if (p->bmem.failed) {
+      p->bmem.release();
+      return fail(LG_CUDA_ERROR, "device allocation failed (candidate batch)");
+    }
+    p->bcap_k = k;
+    p->bcap_N = N;
+  }
+  CK(cudaMemsetAsync(p->d_bat, 0, sizeof(double) * k * per, p->stream));
+  std::vector<LgEngineArgs> ea((size_t)k);
+  const long Wst = p->dense ? p->d : p->W;  // generator row width of the step table A[N][W][d]
+  for (long c = 0; c < k; ++c) {
+    LgEngineArgs E = engine_args(p, N);
+    double* b = p->d_bat + c * per;
+    E.A = p->d_A + c * N * Wst * p->d;
+    E.plan = p->d_plan + c * N * (p->Kc + 1);
+    E.rtab = p->d_rtab ? p->d_rtab + c * N * 64 : nullptr;
+    E.fin = reinterpret_cast<double2*>(b);
+    E.run = b + 2 * S * T;
+    E.trp = reinterpret_cast<double2*>(b + 2 * S * T + runsz);
+    E.psiN = p->d_bpsi + c * T * p->d;
+    E.cl_acs = 0;
+    E.trace = nullptr;
+    ea[c] = E;
+  }
+  CK(cudaMemcpyAsync(p->d_bEA, ea.data(), sizeof(LgEngineArgs) * k, cudaMemcpyHostToDevice, p->stream));
+  void* bargs[] = {&p->d_bEA};
+  cudaError_t e;
+  if (p->engine == 5) {
+    void* f = lg_cl_kernel(3, p->W, p->cl_maxc, p->cl_small);
+    if (!f) return fail(LG_UNSUPPORTED, "no batched forward kernel for this cluster layout");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p->n_groups * p->cl_CS, (unsigned)k);
+    cfg.blockDim = dim3(p->threads);
+    cfg.dynamicSmemBytes = p->cl_smem;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p->cl_CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ensure_smem(f, cfg.dynamicSmemBytes);
+    if (p->cl_CS > 8) cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ++g_launches;
+    e = cudaLaunchKernelExC(&cfg, f, bargs);
+  } else {
+    void* f = lg_ws_kernel(3, p->dense ? -lg_ws_dense_width((int)p->d) : p->W, p->ws_rpl);
+    if (!f) return fail(LG_UNSUPPORTED, "no batched forward kernel for this problem");
+    ensure_smem(f, p->ws_fwd_smem);
+    ++g_launches;
+    e = cudaLaunchKernel(f, dim3(p->n_groups * p->n_slabs, (unsigned)k), dim3(p->threads), bargs, p->ws_fwd_smem,
+                         p->stream);
+  }
+  if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("batched forward launch: ") + cudaGetErrorString(e));
+  for (long c = 0; c < k; ++c) {
+    const double* b = p->d_bat + c * per;
+    LgFinalArgs F = final_args(p, N, p->d_ip, reinterpret_cast<const double2*>(b), b + 2 * S * T,
+                               reinterpret_cast<const double2*>(b + 2 * S * T + runsz), p->d_grad, p->d_bcost + c);
+    F.Kc = 0;  // cost only
+    void* fargs[] = {&F};
+    rc = launch(lg_finalize_kernel(), dim3(1), dim3(32), fargs, 0, p->stream);
+    if (rc) return rc;
+  }
+  CK(cudaMemcpyAsync(costs, p->d_bcost, sizeof(double) * k, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return LG_OK;
+}
+
 int lg_forward_states(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* out) {
   int rc = check_field(p, n_steps, dt, amps);
   if (rc) return rc;

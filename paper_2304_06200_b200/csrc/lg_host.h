@@ -167,6 +167,14 @@ struct lg_problem {
   int live_peak = 0;
   long shard_b = 0, shard_e = 1L << 40;
   // device: static
+  // line-search batch (lg_cost_batch): per-candidate raw outputs [k][fin | run | trp], final
+  // states, costs and engine arguments
+  DevMem bmem;
+  long bcap_k = 0, bcap_N = 0;
+  double* d_bat = nullptr;
+  double2* d_bpsi = nullptr;
+  double* d_bcost = nullptr;
+  LgEngineArgs* d_bEA = nullptr;
   DevMem mem;
   cudaStream_t stream = nullptr;
   int *d_rowlen = nullptr, *d_cols = nullptr, *d_src_s = nullptr, *d_src_c = nullptr, *d_colptr = nullptr,

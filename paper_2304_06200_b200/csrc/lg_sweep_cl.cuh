@@ -525,7 +525,7 @@ __device__ __forceinline__ double2 pen_apply(const LgEngineArgs& E, const LgSpec
 
 // ------------------------------------------------------------------------------------------ forward
 template <int W, int MAXC, bool SMALL>
-__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __grid_constant__ LgEngineArgs E) {
+__device__ __forceinline__ void cl_forward_body(const LgEngineArgs& E) {
   const int g = blockIdx.x / (int)cl_size();
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
@@ -608,6 +608,16 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __
     }
   if (c.own) E.psiN[(long)t0 * c.d + c.orig] = psi;
   cl_sync();
+}
+
+template <int W, int MAXC, bool SMALL>
+__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward(const __grid_constant__ LgEngineArgs E) {
+  cl_forward_body<W, MAXC, SMALL>(E);
+}
+// line-search batch: candidate field blockIdx.y (lg_cost_batch)
+template <int W, int MAXC, bool SMALL>
+__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward_batch(const LgEngineArgs* __restrict__ EA) {
+  cl_forward_body<W, MAXC, SMALL>(EA[blockIdx.y]);
 }
 
 // ------------------------------------------------------------------------------------------ backward
@@ -846,10 +856,15 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
     }                                                                                                    \
     return nullptr;                                                                                      \
   }
+// backward: 0 forward, 1 backward, 3 forward line-search batch
 #define LG_CL_CASE(W_, C_)                                                                                   \
   case C_ * 2:                                                                                               \
+    if (backward == 3) return (void*)lg_k_cl_forward_batch<W_, C_, false>;                                  \
     return backward ? (void*)lg_k_cl_backward<W_, C_, false> : (void*)lg_k_cl_forward<W_, C_, false>;        \
   case C_ * 2 + 1:                                                                                           \
-    if (small == 2) return backward ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;                 \
-    if (small == 3) return backward ? (void*)lg_k_cll_backward<W_, C_, 2> : (void*)lg_k_cll_forward<W_, C_, 2>;\
+    if (small == 2) return backward == 1 ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;            \
+    if (small == 3)                                                                                          \
+      return backward == 3 ? (void*)lg_k_cll_forward_batch<W_, C_, 2>                                        \
+                           : backward ? (void*)lg_k_cll_backward<W_, C_, 2> : (void*)lg_k_cll_forward<W_, C_, 2>; \
+    if (backward == 3) return (void*)lg_k_cl_forward_batch<W_, C_, true>;                                   \
     return backward ? (void*)lg_k_cl_backward<W_, C_, true> : (void*)lg_k_cl_forward<W_, C_, true>;

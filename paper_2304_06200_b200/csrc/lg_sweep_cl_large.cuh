@@ -288,7 +288,7 @@ __device__ __forceinline__ void chain_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, 
 
 // ------------------------------------------------------------------------------------ forward
 template <int W, int MAXC, int RPT>
-__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_forward(const __grid_constant__ LgEngineArgs E) {
+__device__ __forceinline__ void cll_forward_body(const LgEngineArgs& E) {
   const int g = blockIdx.x / (int)cl_size();
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
@@ -378,6 +378,16 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_forward(const __grid_c
   for (int r = 0; r < RPT; ++r)
     if (c.own(r)) E.psiN[(long)t0 * c.d + c.orig(r)] = psi[r];
   cl_sync();
+}
+
+template <int W, int MAXC, int RPT>
+__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_forward(const __grid_constant__ LgEngineArgs E) {
+  cll_forward_body<W, MAXC, RPT>(E);
+}
+// line-search batch: candidate field blockIdx.y (lg_cost_batch)
+template <int W, int MAXC, int RPT>
+__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_forward_batch(const LgEngineArgs* __restrict__ EA) {
+  cll_forward_body<W, MAXC, RPT>(EA[blockIdx.y]);
 }
 
 // ----------------------------------------------------------------------------------- backward

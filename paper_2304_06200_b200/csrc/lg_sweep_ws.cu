@@ -455,7 +455,6 @@ __device__ __forceinline__ double2 pen_row(int d, int Wp, int pen, const int* pc
 
 }  // namespace
 
-extern "C" __global__ void lg_ws_dummy() {}
 
 // Stage the targets / penalty operators of this set into shared memory.
 __device__ __forceinline__ void stage_specs(const LgEngineArgs& E, const WsLay& L, int set, int trel, int I, int Wp,
@@ -478,7 +477,7 @@ __device__ __forceinline__ void stage_specs(const LgEngineArgs& E, const WsLay& 
 // warps 0-1: propagation team P; warps 2-3: per-step scalars team F.  d <= 64.
 // DNS: dense rows (W unused), A_n staged in shared memory one step ahead.
 template <int W, int DNS>
-__global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant__ LgEngineArgs E) {
+__device__ __forceinline__ void ws_forward_body(const LgEngineArgs& E) {
   const int d = E.d, g = blockIdx.x, N = E.N, dd = d * d;
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set];
@@ -604,6 +603,17 @@ __global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant_
         if (kind == LGK_STATE_PEN || kind == LGK_STATE_RUN) E.run[(long)sidx * E.T_total + t0] += runacc[si];
       }
   }
+}
+
+template <int W, int DNS>
+__global__ void __launch_bounds__(128, 1) lg_k_ws_forward(const __grid_constant__ LgEngineArgs E) {
+  ws_forward_body<W, DNS>(E);
+}
+// Line-search batch (lg_cost_batch): candidate field blockIdx.y with its own step generators,
+// plans and raw outputs, all candidates in one launch (src/optimizer.py:153-170).
+template <int W, int DNS>
+__global__ void __launch_bounds__(128, 1) lg_k_ws_forward_batch(const LgEngineArgs* __restrict__ EA) {
+  ws_forward_body<W, DNS>(EA[blockIdx.y]);
 }
 
 // ------------------------------------------------------------------------------------------ backward
@@ -1241,12 +1251,15 @@ extern "C" int lg_ws_layout_words(int d, int nteams, int I, int Wp, int extra_ba
 extern "C" void* lg_ws_kernel(int backward, int W, int rpl) {
   (void)rpl;
 #define LG_WSD(DM_) \
-  if (W == -DM_) return backward == 2 ? (void*)lg_k_wsc_backward<DM_, 1> : (backward ? nullptr : (void*)lg_k_ws_forward<DM_, 1>);
+  if (W == -DM_)                                                                                                 \
+    return backward == 3 ? (void*)lg_k_ws_forward_batch<DM_, 1>                                                  \
+                         : backward == 2 ? (void*)lg_k_wsc_backward<DM_, 1> : (backward ? nullptr : (void*)lg_k_ws_forward<DM_, 1>);
   LG_WSD(8) LG_WSD(16) LG_WSD(32) LG_WSD(40) LG_WSD(48) LG_WSD(64)
 #undef LG_WSD
 #define LG_WS(W_)                                                                               \
   if (W == W_)                                                                                  \
-    return backward == 2 ? (void*)lg_k_wsc_backward<W_, 0>                                      \
+    return backward == 3 ? (void*)lg_k_ws_forward_batch<W_, 0>                                  \
+                         : backward == 2 ? (void*)lg_k_wsc_backward<W_, 0>                      \
                          : (backward ? (void*)lg_k_ws_backward<W_> : (void*)lg_k_ws_forward<W_, 0>);
   LG_WS(1) LG_WS(2) LG_WS(3) LG_WS(4) LG_WS(5) LG_WS(6) LG_WS(7) LG_WS(8) LG_WS(9)
 #undef LG_WS
