@@ -102,7 +102,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     bsm = p->ws_bwd_smem;
     bblock = dim3(p->ws_bwd_threads);
   }
-  auto cl_launch = [&](void* f, bool backward) -> int {
+  auto cl_launch = [&](void* f, bool backward, int clusters = 0) -> int {
     E.cl_acs = backward ? p->cl_acs : 0;
     const bool split = backward && p->cl_split;
     E.cl_R = split ? p->cl_R_b : p->cl_R;
@@ -110,7 +110,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     E.cl_E = split ? p->cl_E_b : p->cl_E;
     if (split) f = lg_cl_kernel(1, p->W, p->cl_maxc, 2);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p->n_groups * p->cl_CS);
+    cfg.gridDim = dim3((clusters ? clusters : p->n_groups) * p->cl_CS);
     cfg.blockDim = dim3(split ? p->cl_T_b : p->threads);
     cfg.dynamicSmemBytes = split ? p->cl_smem_split : (backward ? p->cl_smem_b : p->cl_smem);
     cfg.stream = p->stream;
@@ -145,7 +145,33 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     rc = launch(lg_trsum_kernel(), dim3((unsigned)((cnt + 255) / 256)), dim3(256), targs, 0, p->stream);
     if (rc) return rc;
     if (p->engine == 5) {
-      rc = cl_launch(bwd, true);
+      // LARGE kernels: two-phase backward when the psi_{n-1} / lambda_s(n) store fits in HBM
+      bool two = p->cl_small == 3 && p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");
+      if (two) {
+        const long need = (long)p->n_groups * N * p->d;
+        if (need > p->bk_cap) {
+          p->bkmem.release();
+          p->bk_cap = 0;
+          p->d_bk_psi = p->bkmem.alloc<double2>((size_t)need);
+          p->d_bk_lam = p->bkmem.alloc<double2>((size_t)need * std::max(p->cta_Imax, 1));
+          if (p->bkmem.failed) {
+            p->bkmem.release();
+          } else {
+            p->bk_cap = need;
+          }
+        }
+        two = p->bk_cap >= need;
+      }
+      if (two) {
+        E.bk_psi = p->d_bk_psi;
+        E.bk_lam = p->d_bk_lam;
+        rc = cl_launch(lg_cl_kernel(4, p->W, p->cl_maxc, 3), true);
+        if (rc) return rc;
+        rc = cl_launch(lg_cl_kernel(5, p->W, p->cl_maxc, 3), true,
+                       (int)std::min<long>(p->cl_aux_ncl, (long)p->n_groups * N));
+      } else {
+        rc = cl_launch(bwd, true);
+      }
       if (rc) return rc;
     } else if (p->engine == 4 && p->ws_cluster) {
       cudaLaunchConfig_t cfg{};
@@ -365,7 +391,10 @@ const char* lg_engine_name(lg_problem* p) {
     case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
     case 5:
       return p->cl_split ? "cluster-split:lg_k_cl_backward"
-                         : (p->cl_small >= 3 ? "cluster-large:lg_k_cll_backward" : "cluster:lg_k_cl_backward");
+                         : (p->cl_small >= 3 ? (p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED")
+                                                    ? "cluster-large:lg_k_cll_adjoint+lg_k_cll_aux"
+                                                    : "cluster-large:lg_k_cll_backward")
+                                              : "cluster:lg_k_cl_backward");
     default: return "unknown";
   }
 }

@@ -332,6 +332,33 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_Q = Q;
   p->cl_E = E;
   p->cl_small = small;
+  p->cl_aux_ncl = 0;
+  if (small == 3) {  // two-phase backward: adjoint sweep + derivative-product items on every resident cluster
+    void* fa = lg_cl_kernel(4, p->W, maxc, 3);
+    void* fi = lg_cl_kernel(5, p->W, maxc, 3);
+    int ncl = 0;
+    if (fa && fi && cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) == cudaSuccess &&
+        cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) == cudaSuccess &&
+        (CS <= 8 || (cudaFuncSetAttribute(fa, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                     cudaFuncSetAttribute(fi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess))) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = words_b * 16;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&ncl, fi, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        ncl = 0;
+      }
+    }
+    p->cl_aux_ncl = ncl;
+  }
   p->cl_maxc = maxc;
   p->cl_smem = words * 16;
   p->cl_smem_b = words_b * 16;

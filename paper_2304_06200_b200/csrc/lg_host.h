@@ -159,6 +159,10 @@ struct lg_problem {
   // cluster engine
   int cl_split = 0, cl_R_b = 0, cl_Q_b = 1, cl_E_b = 0, cl_T_b = 0, cl_smem_split = 0;  // split backward
   int cl_CS = 0, cl_R = 0, cl_H = 0, cl_Q = 1, cl_E = 0, cl_small = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
+  int cl_aux_ncl = 0;  // LARGE two-phase backward: co-resident clusters of the item kernel (0: fused backward)
+  DevMem bkmem;        // ... its psi_{n-1} / lambda_s(n) store
+  long bk_cap = 0;
+  double2 *d_bk_psi = nullptr, *d_bk_lam = nullptr;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
   unsigned char* d_cl_slot = nullptr;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
@@ -240,6 +244,8 @@ struct lg_problem {
       if (e) cudaEventDestroy(e);
     nmem.release();
     dtmem.release();
+    bmem.release();
+    bkmem.release();
     mem.release();
     if (d_splitws) cudaFree(d_splitws);
     if (stream && own_stream) cudaStreamDestroy(stream);

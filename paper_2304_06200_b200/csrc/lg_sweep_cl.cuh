@@ -856,15 +856,20 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
     }                                                                                                    \
     return nullptr;                                                                                      \
   }
-// backward: 0 forward, 1 backward, 3 forward line-search batch
+// backward: 0 forward, 1 backward, 3 forward line-search batch; LARGE only: 4 adjoint sweep storing
+// psi_{n-1} / lambda_s(n), 5 derivative-product items
 #define LG_CL_CASE(W_, C_)                                                                                   \
   case C_ * 2:                                                                                               \
     if (backward == 3) return (void*)lg_k_cl_forward_batch<W_, C_, false>;                                  \
+    if (backward >= 4) return nullptr;                                                                       \
     return backward ? (void*)lg_k_cl_backward<W_, C_, false> : (void*)lg_k_cl_forward<W_, C_, false>;        \
   case C_ * 2 + 1:                                                                                           \
     if (small == 2) return backward == 1 ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;            \
+    if (backward >= 4 && small != 3) return nullptr;                                                         \
     if (small == 3)                                                                                          \
       return backward == 3 ? (void*)lg_k_cll_forward_batch<W_, C_, 2>                                        \
-                           : backward ? (void*)lg_k_cll_backward<W_, C_, 2> : (void*)lg_k_cll_forward<W_, C_, 2>; \
+           : backward == 4 ? (void*)lg_k_cll_adjoint<W_, C_, 2>                                              \
+           : backward == 5 ? (void*)lg_k_cll_aux<W_, C_, 2>                                                  \
+           : backward      ? (void*)lg_k_cll_backward<W_, C_, 2> : (void*)lg_k_cll_forward<W_, C_, 2>;        \
     if (backward == 3) return (void*)lg_k_cl_forward_batch<W_, C_, true>;                                   \
     return backward ? (void*)lg_k_cl_backward<W_, C_, true> : (void*)lg_k_cl_forward<W_, C_, true>;

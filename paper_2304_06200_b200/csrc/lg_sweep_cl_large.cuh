@@ -391,14 +391,67 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_forward_batch(const Lg
 }
 
 // ----------------------------------------------------------------------------------- backward
+// Derivative products of step n (src/costs.py:328-339): for every channel group with a common aux
+// plan, the aux chain [top_k ... | bottom] on the bottom psi_{n-1}, then <lambda_s(n)|top_k> into ip.
 template <int W, int MAXC, int RPT>
-__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_constant__ LgEngineArgs E) {
-  const int g = blockIdx.x / (int)cl_size();
-  const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
-  const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
-  const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
-  ClL c = make_cll<RPT>(E, cmax, true);
-  ClLRegs<W, MAXC, RPT> R;
+__device__ __forceinline__ void aux_products_l(const LgEngineArgs& E, const ClL& c, ClLRegs<W, MAXC, RPT>& R, int n,
+                                               int set, int t0, const double2 (&psip)[RPT],
+                                               const double2 (&lam)[RPT][LG_MAX_SPECS]) {
+  const int I = E.set_nspec[set], Kc = E.Kc;
+  const int4* pln = E.plan + (long)n * (Kc + 1);
+  int gch[LG_MAX_CHANNELS];
+  unsigned done = 0;
+  for (int kc = 0; kc < Kc; ++kc) {
+    if (done & (1u << kc)) continue;
+    const int4 pk = pln[1 + kc];
+    int G = 0;
+    for (int k2 = kc; k2 < Kc; ++k2) {
+      const int4 p2 = pln[1 + k2];
+      if (!(done & (1u << k2)) && p2.x == pk.x && p2.y == pk.y) {
+        gch[G++] = k2;
+        done |= 1u << k2;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      if (c.slot(r)) {
+        for (int q = 0; q < G; ++q) put_l(c, c.tb0, q, make_double2(0.0, 0.0), r);
+        put_l(c, c.tb0, G, psip[r], r);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) R.cur[r][q] = q == G ? psip[r] : make_double2(0.0, 0.0);
+    }
+    if ((int)threadIdx.x < G)  // channel offsets of the top columns (read after chain_l's cluster barrier)
+      reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] = gch[threadIdx.x] * 2 * RPT * c.T;
+    chain_l(c, R, G + 1, 1, pk.x, pk.y, 1.0);
+    double2 v[16];
+    const int nv = I * G;
+    for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      if (c.own(r))
+        for (int gi = 0; gi < G; ++gi)
+          for (int si = 0; si < I; ++si) {
+            double2 dd = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < MAXC; ++q)
+              if (q == gi) dd = R.cur[r][q];
+            v[gi * I + si] = cadd(v[gi * I + si], cdot(lam[r][si], dd));
+          }
+    cll_reduce<16>(c, v, nv);
+    if (c.rank == 0 && threadIdx.x == 0)
+      for (int gi = 0; gi < G; ++gi)
+        for (int si = 0; si < I; ++si) {
+          const int sidx = E.set_spec[set][si];
+          E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + t0] = v[gi * I + si];
+        }
+  }
+}
+
+// kernel prologue shared by the backward kernels: gather offsets, zeroed windows, exchange
+// mbarriers, control rows staged (padded to two entries per row, Wc <= 2)
+template <int W, int MAXC, int RPT>
+__device__ __forceinline__ void cll_backward_setup(const LgEngineArgs& E, const ClL& c, ClLRegs<W, MAXC, RPT>& R) {
   load_go_l(E, c, R);
   for (int q = threadIdx.x; q < c.tb1 + c.CST * c.WIN; q += blockDim.x) cl_sm[q] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
@@ -406,7 +459,7 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_
     mb_init(cll_mb(c, 1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int kw = 0; kw < Kc * 2; ++kw)  // control rows padded to two entries per row (Wc <= 2)
+  for (int kw = 0; kw < E.Kc * 2; ++kw)
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int k = kw >> 1, w = kw & 1;
@@ -417,6 +470,21 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_
           ok ? E.cl_accols[src + c.gi(r)] - c.g0 + c.H : c.H + (c.slot(r) ? c.lr(r) : 0);
     }
   cl_sync();
+}
+
+// STORE == false: the fused backward sweep.  STORE == true: the adjoint sweep only -- psi_{n-1}
+// and lambda_s(n) of every step go to HBM (E.bk_psi / E.bk_lam, renumbered rows) and the
+// derivative products run afterwards as independent (step, trajectory) items on every resident
+// cluster (lg_k_cll_aux): no tail wave, and the aux chains no longer wait on the adjoint chain.
+template <int W, int MAXC, int RPT, bool STORE>
+__device__ __forceinline__ void cll_backward_body(const LgEngineArgs& E) {
+  const int g = blockIdx.x / (int)cl_size();
+  const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
+  const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
+  const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
+  ClL c = make_cll<RPT>(E, cmax, true);
+  ClLRegs<W, MAXC, RPT> R;
+  cll_backward_setup(E, c, R);
   bool anypen = false, anyrun = false;
   for (int si = 0; si < I; ++si) {
     const int k = E.spec[E.set_spec[set][si]].kind;
@@ -472,7 +540,6 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_
       }
     cl_sync();
   }
-  int gch[LG_MAX_CHANNELS];
   for (int n = N - 1; n >= 0; --n) {
     const int4* pln = E.plan + (long)n * (Kc + 1);
     const int4 pl = pln[0];
@@ -498,52 +565,17 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_
       for (int q = 1; q < MAXC; ++q)
         if (q - 1 < LG_MAX_SPECS) lamn[r][q - 1] = R.cur[r][q];
     }
-    // derivative products per channel group (src/costs.py:328-339)
-    unsigned done = 0;
-    for (int kc = 0; kc < Kc; ++kc) {
-      if (done & (1u << kc)) continue;
-      const int4 pk = pln[1 + kc];
-      int G = 0;
-      for (int k2 = kc; k2 < Kc; ++k2) {
-        const int4 p2 = pln[1 + k2];
-        if (!(done & (1u << k2)) && p2.x == pk.x && p2.y == pk.y) {
-          gch[G++] = k2;
-          done |= 1u << k2;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        if (c.slot(r)) {
-          for (int q = 0; q < G; ++q) put_l(c, c.tb0, q, make_double2(0.0, 0.0), r);
-          put_l(c, c.tb0, G, psip[r], r);
-        }
-#pragma unroll
-        for (int q = 0; q < MAXC; ++q) R.cur[r][q] = q == G ? psip[r] : make_double2(0.0, 0.0);
-      }
-      if ((int)threadIdx.x < G)  // channel offsets of the top columns (read after chain_l's cluster barrier)
-        reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] = gch[threadIdx.x] * 2 * RPT * c.T;
-      chain_l(c, R, G + 1, 1, pk.x, pk.y, 1.0);
-      double2 v[16];
-      const int nv = I * G;
-      for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);
+    if constexpr (STORE) {  // hand psi_{n-1} and lambda_s(n) to the item kernel
+      double2* bp = E.bk_psi + ((long)g * N + n) * c.d;
+      double2* bl = E.bk_lam + ((long)g * N + n) * E.cta_Imax * c.d;
 #pragma unroll
       for (int r = 0; r < RPT; ++r)
-        if (c.own(r))
-          for (int gi = 0; gi < G; ++gi)
-            for (int si = 0; si < I; ++si) {
-              double2 dd = make_double2(0.0, 0.0);
-#pragma unroll
-              for (int q = 0; q < MAXC; ++q)
-                if (q == gi) dd = R.cur[r][q];
-              v[gi * I + si] = cadd(v[gi * I + si], cdot(lam[r][si], dd));
-            }
-      cll_reduce<16>(c, v, nv);
-      if (c.rank == 0 && threadIdx.x == 0)
-        for (int gi = 0; gi < G; ++gi)
-          for (int si = 0; si < I; ++si) {
-            const int sidx = E.set_spec[set][si];
-            E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + t0] = v[gi * I + si];
-          }
+        if (c.own(r)) {
+          bp[c.gi(r)] = psip[r];
+          for (int si = 0; si < I; ++si) bl[(long)si * c.d + c.gi(r)] = lam[r][si];
+        }
+    } else {
+      aux_products_l(E, c, R, n, set, t0, psip, lam);
     }
     if (n == 0) break;
     // costate sources at psi_{n-1} (src/costs.py:341-353, :474-479)
@@ -584,6 +616,44 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_
       psi[r] = psip[r];
     }
     cl_sync();
+  }
+  cl_sync();
+}
+
+template <int W, int MAXC, int RPT>
+__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_backward(const __grid_constant__ LgEngineArgs E) {
+  cll_backward_body<W, MAXC, RPT, false>(E);
+}
+template <int W, int MAXC, int RPT>
+__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_adjoint(const __grid_constant__ LgEngineArgs E) {
+  cll_backward_body<W, MAXC, RPT, true>(E);
+}
+// Derivative products as independent items (step n, trajectory group g), item = k * n_groups + g
+// with k = N - 1 - n (the trajectories of one step are neighbours: A_n is read once into L2), dealt
+// round-robin to the grid's clusters (all co-resident).  Reads psi_{n-1} and lambda_s(n) from HBM.
+template <int W, int MAXC, int RPT>
+__global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_aux(const __grid_constant__ LgEngineArgs E) {
+  const int cid = blockIdx.x / (int)cl_size(), ncl = gridDim.x / (int)cl_size();
+  const int Kc = E.Kc, N = E.N;
+  const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
+  ClL c = make_cll<RPT>(E, cmax, true);
+  ClLRegs<W, MAXC, RPT> R;
+  cll_backward_setup(E, c, R);
+  const long items = (long)E.n_groups * N;
+  for (long it = cid; it < items; it += ncl) {
+    const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
+    const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
+    load_row_l(E, c, n, R);
+    const double2* bp = E.bk_psi + ((long)g * N + n) * c.d;
+    const double2* bl = E.bk_lam + ((long)g * N + n) * E.cta_Imax * c.d;
+    double2 psip[RPT], lam[RPT][LG_MAX_SPECS];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      psip[r] = c.own(r) ? bp[c.gi(r)] : make_double2(0.0, 0.0);
+      for (int si = 0; si < LG_MAX_SPECS; ++si)
+        lam[r][si] = c.own(r) && si < I ? bl[(long)si * c.d + c.gi(r)] : make_double2(0.0, 0.0);
+    }
+    aux_products_l(E, c, R, n, set, t0, psip, lam);
   }
   cl_sync();
 }
