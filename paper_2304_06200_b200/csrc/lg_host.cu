@@ -378,6 +378,7 @@ LgEngineArgs engine_args(lg_problem* p, long N) {
   E.cl_cols = p->d_cl_cols;
   E.cl_slot = p->d_cl_slot;
   E.cl_accols = p->d_cl_accols;
+  E.cl_cshare = p->cl_cshare;
   if (std::getenv("LG_TRACE") && p->engine == 4) {
     static long long* tbuf = nullptr;
     static size_t tcap = 0;

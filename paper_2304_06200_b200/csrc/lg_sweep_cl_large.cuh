@@ -191,6 +191,30 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
     for (int q = 0; q < NC; ++q) p[q] = make_double2(0.0, 0.0);
 #pragma unroll
     for (int q = 0; q < (SPL ? NC : 1); ++q) pq[q] = make_double2(0.0, 0.0);
+    if (MODE >= 1 && !(c.dbg & 1)) {  // A_c of each top's channel times the bottom column (src/derivatives.py:154-164)
+      // two staged entries per (channel, row) (the second zero when Wc == 1).  MODE 2: the tops come
+      // in pairs of channels with one column pattern (c4: x and y drive of a transmon), and each
+      // pair shares its two bottom-column gathers.
+      const int* tab = reinterpret_cast<const int*>(cl_sm + c.rt + 64);
+      const int* accb = reinterpret_cast<const int*>(cl_sm + c.accs) + c.lr(rr);
+      constexpr int STEP = MODE == 2 ? 2 : 1;
+#pragma unroll
+      for (int q = 0; q < NC - 1; q += STEP) {
+        const int koff = tab[q];
+        double2 xb[2];
+        {
+          const int o0 = accb[koff], o1 = accb[koff + RPT * c.T];
+          xb[0] = cl_sm[widx(c, X, o0, NC - 1)];
+          xb[1] = cl_sm[widx(c, X, o1, NC - 1)];
+        }
+#pragma unroll
+        for (int h = 0; h < STEP; ++h) {
+          const double2* ac = cl_sm + c.acs + tab[q + h] + c.lr(rr);
+          cmac(p[q + h], pq[SPL ? q + h : 0], ac[0], xb[0], SPL);
+          cmac(p[q + h], pq[SPL ? q + h : 0], ac[RPT * c.T], xb[1], SPL);
+        }
+      }
+    }
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const int k = rr * W + w;
@@ -199,26 +223,6 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
       const double2 a = R.a[rr][w];
 #pragma unroll
       for (int q = 0; q < NC; ++q) cmac(p[q], pq[SPL ? q : 0], a, xr[q], SPL);
-    }
-    if (MODE == 1 && !(c.dbg & 1)) {  // A_c of each top's channel times the bottom column (src/derivatives.py:154-164)
-      // two staged entries per (channel, row) (the second zero when Wc == 1); offsets first, so
-      // the dependent value / gather loads of all tops are in flight together
-      int off[NC > 1 ? NC - 1 : 1][2];
-#pragma unroll
-      for (int q = 0; q < NC - 1; ++q) {
-        const int koff = reinterpret_cast<const int*>(cl_sm + c.rt + 64)[q] + c.lr(rr);
-        const int* acc = reinterpret_cast<const int*>(cl_sm + c.accs) + koff;
-        off[q][0] = acc[0];
-        off[q][1] = acc[RPT * c.T];
-      }
-#pragma unroll
-      for (int q = 0; q < NC - 1; ++q) {
-        const int koff = reinterpret_cast<const int*>(cl_sm + c.rt + 64)[q] + c.lr(rr);
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          cmac(p[q], pq[SPL ? q : 0], cl_sm[c.acs + koff + w * RPT * c.T], cl_sm[widx(c, X, off[q][w], NC - 1)], SPL);
-        }
-      }
     }
     // local stores of this row (plain shared stores; the halo pushes follow for all rows)
     double2* yr = cl_sm + widx(c, Y, c.H + c.lr(rr), 0);
@@ -276,7 +280,12 @@ __device__ __forceinline__ void chain_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, 
     if (C == n) {                                  \
       if (mode == 0)                               \
         chain_l_nc<W, MAXC, RPT, n, 0>(c, R, m, s);     \
-      else if constexpr (n >= 2)                   \
+      else if constexpr (n >= 3 && n % 2 == 1) {   \
+        if (mode == 2)                             \
+          chain_l_nc<W, MAXC, RPT, n, 2>(c, R, m, s);   \
+        else                                       \
+          chain_l_nc<W, MAXC, RPT, n, 1>(c, R, m, s);   \
+      } else if constexpr (n >= 2)                 \
         chain_l_nc<W, MAXC, RPT, n, 1>(c, R, m, s);     \
     }
   LG_NCL(1) LG_NCL(2) LG_NCL(3) LG_NCL(4) LG_NCL(5) LG_NCL(6) LG_NCL(7) LG_NCL(8)
@@ -423,7 +432,10 @@ __device__ __forceinline__ void aux_products_l(const LgEngineArgs& E, const ClL&
     }
     if ((int)threadIdx.x < G)  // channel offsets of the top columns (read after chain_l's cluster barrier)
       reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] = gch[threadIdx.x] * 2 * RPT * c.T;
-    chain_l(c, R, G + 1, 1, pk.x, pk.y, 1.0);
+    bool pairs = G % 2 == 0 && !(E.dbg & 2);  // every pair of tops: consecutive channels, one column pattern
+    for (int q = 0; q + 1 < G && pairs; q += 2)
+      pairs = gch[q + 1] == gch[q] + 1 && ((E.cl_cshare >> gch[q + 1]) & 1u);
+    chain_l(c, R, G + 1, pairs ? 2 : 1, pk.x, pk.y, 1.0);
     double2 v[16];
     const int nv = I * G;
     for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);

@@ -121,6 +121,7 @@ struct LgEngineArgs {
   const double2* diag_D;
   int cl_acs;               // backward stages the control-generator rows in shared memory
   int dbg;                  // LG_DBG bits (timing experiments only; results are wrong when set)
+  unsigned cl_cshare;       // bit k: control channel k has channel k-1's column pattern (LARGE aux chains)
   double2* bk_psi;          // cluster LARGE two-phase backward: psi_{n-1} [group][N][d] (renumbered rows)
   double2* bk_lam;          // ... lambda_s(n) [group][N][cta_Imax][d]
   int ws_nw;                // ws cluster backward: derivative workers per control channel

@@ -78,3 +78,32 @@ def test_dense_goldens_with_forced_gemm_tiles(n32, splitk, monkeypatch):
                          (CostKind.GATE_RUNNING_INFIDELITY, "cost_g3", "grad_g3")]:
         t = [CostTerm(kind, 1.0, target_images=zs["images"])]
         _check(NativeProblem(prob, t, basis=zs["basis"]).grad(a), zs[ck], zs[gk])
+
+
+def test_c4_full_size_engine_agreement(monkeypatch):
+    """c4 at FULL size (d = 10^4, K = 32, N = 4000; the reference needs ~21 h, so no golden): the
+    bench configuration evaluated three ways must agree -- the LARGE kernels' two-phase backward
+    (default), their fused backward (LG_CL_FUSED=1: bit-identical, the same chains on the same
+    psi_{n-1} / lambda(n) values) and the generic cluster kernels (LG_CL_NOLARGE=1: another
+    summation order, so 1e-12 / 1e-10) -- and composite_cost must equal composite_grad's cost
+    bitwise.  The prefix golden (c4.npz, N' = 8, all 32 states) pins the same code path against
+    the reference."""
+    case = models.build_case("c4")
+
+    def run():
+        npb = NativeProblem(case.problem, case.terms, basis=case.problem.basis)
+        return npb.engine, npb.grad(case.field), npb.cost(case.field)
+
+    eng, res, cost = run()
+    assert eng.startswith("cluster-large:lg_k_cll_adjoint"), eng
+    assert cost == res.cost
+    monkeypatch.setenv("LG_CL_FUSED", "1")
+    eng_f, res_f, _ = run()
+    assert eng_f.startswith("cluster-large:lg_k_cll_backward"), eng_f
+    assert res_f.cost == res.cost and np.array_equal(res_f.grad, res.grad)
+    monkeypatch.delenv("LG_CL_FUSED")
+    monkeypatch.setenv("LG_CL_NOLARGE", "1")
+    eng_g, res_g, _ = run()
+    assert eng_g.startswith("cluster:"), eng_g
+    assert abs(res_g.cost - res.cost) <= COST_TOL
+    assert G.grad_rel(res_g.grad, res.grad) <= 1e-10
