@@ -102,9 +102,9 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     bsm = p->ws_bwd_smem;
     bblock = dim3(p->ws_bwd_threads);
   }
-  auto cl_launch = [&](void* f, bool backward, int clusters = 0) -> int {
+  auto cl_launch = [&](void* f, bool backward, int clusters = 0, bool allow_split = true) -> int {
     E.cl_acs = backward ? p->cl_acs : 0;
-    const bool split = backward && p->cl_split;
+    const bool split = backward && p->cl_split && allow_split;
     E.cl_R = split ? p->cl_R_b : p->cl_R;
     E.cl_Q = split ? p->cl_Q_b : p->cl_Q;
     E.cl_E = split ? p->cl_E_b : p->cl_E;
@@ -146,7 +146,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     if (rc) return rc;
     if (p->engine == 5) {
       // LARGE kernels: two-phase backward when the psi_{n-1} / lambda_s(n) store fits in HBM
-      bool two = p->cl_small == 3 && p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");
+      bool two = p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");
       if (two) {
         const long need = (long)p->n_groups * N * p->d;
         if (need > p->bk_cap) {
@@ -165,10 +165,10 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
       if (two) {
         E.bk_psi = p->d_bk_psi;
         E.bk_lam = p->d_bk_lam;
-        rc = cl_launch(lg_cl_kernel(4, p->W, p->cl_maxc, 3), true);
+        rc = cl_launch(lg_cl_kernel(4, p->W, p->cl_maxc, p->cl_small), true, 0, false);
         if (rc) return rc;
-        rc = cl_launch(lg_cl_kernel(5, p->W, p->cl_maxc, 3), true,
-                       (int)std::min<long>(p->cl_aux_ncl, (long)p->n_groups * N));
+        rc = cl_launch(lg_cl_kernel(5, p->W, p->cl_maxc, p->cl_small), true,
+                       (int)std::min<long>(p->cl_aux_ncl, (long)p->n_groups * N), false);
       } else {
         rc = cl_launch(bwd, true);
       }
@@ -389,12 +389,13 @@ const char* lg_engine_name(lg_problem* p) {
     case 2: return "cta:lg_k_cta_backward";
     case 3: return "dense:lg_k_zgemm_taylor";
     case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
-    case 5:
-      return p->cl_split ? "cluster-split:lg_k_cl_backward"
-                         : (p->cl_small >= 3 ? (p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED")
-                                                    ? "cluster-large:lg_k_cll_adjoint+lg_k_cll_aux"
-                                                    : "cluster-large:lg_k_cll_backward")
-                                              : "cluster:lg_k_cl_backward");
+    case 5: {
+      const bool two = p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");
+      if (p->cl_small >= 3)
+        return two ? "cluster-large:lg_k_cll_adjoint+lg_k_cll_aux" : "cluster-large:lg_k_cll_backward";
+      if (two) return "cluster-2phase:lg_k_cl_adjoint+lg_k_cl_aux";
+      return p->cl_split ? "cluster-split:lg_k_cl_backward" : "cluster:lg_k_cl_backward";
+    }
     default: return "unknown";
   }
 }

@@ -340,9 +340,9 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   p->cl_E = E;
   p->cl_small = small;
   p->cl_aux_ncl = 0;
-  if (small == 3) {  // two-phase backward: adjoint sweep + derivative-product items on every resident cluster
-    void* fa = lg_cl_kernel(4, p->W, maxc, 3);
-    void* fi = lg_cl_kernel(5, p->W, maxc, 3);
+  {  // two-phase backward: adjoint sweep + derivative-product items on every resident cluster
+    void* fa = lg_cl_kernel(4, p->W, maxc, small);
+    void* fi = lg_cl_kernel(5, p->W, maxc, small);
     int ncl = 0;
     if (fa && fi && cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) == cudaSuccess &&
         cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, words_b * 16) == cudaSuccess &&

@@ -620,20 +620,75 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_forward_batch(co
   cl_forward_body<W, MAXC, SMALL>(EA[blockIdx.y]);
 }
 
+// Derivative products of step n (src/costs.py:328-339): per channel group with a common aux plan,
+// the aux chain [0 ... 0 | psi_{n-1}] and <lambda_s(n)|top_k> into ip.
+template <int W, int MAXC, bool SMALL>
+__device__ __forceinline__ void aux_products(const LgEngineArgs& E, const Cl& c, ClRegs<W, MAXC, SMALL>& R, int n,
+                                             int set, int t0, double2 psip, const double2 (&lamc)[LG_MAX_SPECS]) {
+  const int I = E.set_nspec[set], Kc = E.Kc;
+  const int4* pln = E.plan + (long)n * (Kc + 1);
+  int gch[LG_MAX_CHANNELS];
+  unsigned done = 0;
+  for (int kc = 0; kc < Kc; ++kc) {
+    if (done & (1u << kc)) continue;
+    const int4 pk = pln[1 + kc];
+    int G = 0;
+    for (int k2 = kc; k2 < Kc; ++k2) {
+      const int4 p2 = pln[1 + k2];
+      if (!(done & (1u << k2)) && p2.x == pk.x && p2.y == pk.y) {
+        gch[G++] = k2;
+        done |= 1u << k2;
+      }
+    }
+    // stage [0 ... 0 | psi_{n-1}]
+    if (c.slot) {
+      for (int q = 0; q < G; ++q) put(c, c.tb0, q, make_double2(0.0, 0.0));
+      put(c, c.tb0, G, psip);
+    }
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) R.cur[q] = q == G ? psip : make_double2(0.0, 0.0);
+    if (threadIdx.x < G)  // channel offsets of the top columns (read by chain() after its cluster barrier)
+      reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] =
+          gch[threadIdx.x] * E.Wc * (c.acs >= 0 ? c.T : c.d);
+    chain<W, MAXC, SMALL>(E, c, R, G + 1, 1, G, pk.x, pk.y, 1.0);
+    double2 v[16];
+    const int nv = I * G;
+    for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);
+    if (c.own)
+      for (int gi = 0; gi < G; ++gi)
+        for (int si = 0; si < I; ++si) {
+          double2 dd = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q)
+            if (q == gi) dd = R.cur[q];
+          v[gi * I + si] = cdot(lamc[si], dd);
+        }
+    cl_reduce<16>(c, v, nv);
+    if (c.rank == 0 && threadIdx.x == 0)
+      for (int gi = 0; gi < G; ++gi)
+        for (int si = 0; si < I; ++si) {
+          const int sidx = E.set_spec[set][si];
+          E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + t0] = v[gi * I + si];
+        }
+  }
+}
+
 // ------------------------------------------------------------------------------------------ backward
 // SPLIT (SMALL only): the cluster's CTAs form two groups over the same row partition -- group 0
 // runs the adjoint chain and the costates, group 1 the aux (derivative) chains and the inner
 // products of step n while group 0 already works on step n - 1.  psi_{n-1} and lambda_s(n) go
 // from each group-0 CTA to its group-1 partner through a hand-off ring (st.async + mbarriers).
-template <int W, int MAXC, bool SMALL, bool SPLIT = false>
-__global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 : 1)
-    lg_k_cl_backward(const __grid_constant__ LgEngineArgs E) {
+// STORE (two-phase backward, not with SPLIT): the adjoint sweep only -- psi_{n-1} and lambda_s(n)
+// of every step go to HBM (E.bk_psi / E.bk_lam, renumbered own rows), and lg_k_cl_aux runs the
+// derivative products as independent (step, trajectory) items on every resident cluster.
+template <int W, int MAXC, bool SMALL, bool SPLIT, bool STORE>
+__device__ __forceinline__ void cl_backward_body(const LgEngineArgs& E) {
   const int g = blockIdx.x / (int)cl_size();
   const int set = E.grp_set[g], t0 = E.grp_t0[g], trel = t0 - E.set_t0[set];
   const int I = E.set_nspec[set], Kc = E.Kc, N = E.N;
   const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
   Cl c = make_cl(E, cmax, cst, W, SPLIT);
-  const bool doA = !SPLIT || c.group == 0, doB = !SPLIT || c.group == 1;
+  const bool doA = !SPLIT || c.group == 0, doB = (!SPLIT || c.group == 1) && !STORE;
   ClRegs<W, MAXC, SMALL> R;
   load_cols<W, MAXC, SMALL>(E, c, R);
   // zero everything up to the end of the window buffers (pad gathers may read a few rows past a
@@ -727,6 +782,10 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
 #pragma unroll
       for (int q = 1; q < MAXC; ++q)
         if (q - 1 < LG_MAX_SPECS) lamn[q - 1] = R.cur[q];
+      if (STORE && c.own) {  // hand psi_{n-1} and lambda_s(n) to the item kernel
+        E.bk_psi[((long)g * N + n) * c.d + c.gi] = psip;
+        for (int si = 0; si < I; ++si) E.bk_lam[(((long)g * N + n) * E.cta_Imax + si) * c.d + c.gi] = lam[si];
+      }
       if (SPLIT) {  // hand psi_{n-1} and lambda_s(n) to the partner CTA of group 1
         if (it >= LG_CL_HR) mb_wait_cluster(cl_mb(c, 3 + LG_CL_HR + hs), (unsigned)((it / LG_CL_HR) - 1) & 1u);
         if (c.slot) {
@@ -753,50 +812,7 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
                            cl_map_u(smaddr(cl_mb(c, 3 + LG_CL_HR + hs)), c.rank))
                        : "memory");
       }
-    // derivative products per channel group (src/costs.py:328-339)
-    unsigned done = 0;
-    for (int kc = 0; kc < Kc; ++kc) {
-      if (done & (1u << kc)) continue;
-      const int4 pk = pln[1 + kc];
-      int G = 0;
-      for (int k2 = kc; k2 < Kc; ++k2) {
-        const int4 p2 = pln[1 + k2];
-        if (!(done & (1u << k2)) && p2.x == pk.x && p2.y == pk.y) {
-          gch[G++] = k2;
-          done |= 1u << k2;
-        }
-      }
-      // stage [0 ... 0 | psi_{n-1}]
-      if (c.slot) {
-        for (int q = 0; q < G; ++q) put(c, c.tb0, q, make_double2(0.0, 0.0));
-        put(c, c.tb0, G, psip);
-      }
-#pragma unroll
-      for (int q = 0; q < MAXC; ++q) R.cur[q] = q == G ? psip : make_double2(0.0, 0.0);
-      if (threadIdx.x < G)  // channel offsets of the top columns (read by chain() after its cluster barrier)
-        reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] =
-            gch[threadIdx.x] * E.Wc * (c.acs >= 0 ? c.T : c.d);
-      chain<W, MAXC, SMALL>(E, c, R, G + 1, 1, G, pk.x, pk.y, 1.0);
-      double2 v[16];
-      const int nv = I * G;
-      for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);
-      if (c.own)
-        for (int gi = 0; gi < G; ++gi)
-          for (int si = 0; si < I; ++si) {
-            double2 dd = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < MAXC; ++q)
-              if (q == gi) dd = R.cur[q];
-            v[gi * I + si] = cdot(lamc[si], dd);
-          }
-      cl_reduce<16>(c, v, nv);
-      if (c.rank == 0 && threadIdx.x == 0)
-        for (int gi = 0; gi < G; ++gi)
-          for (int si = 0; si < I; ++si) {
-            const int sidx = E.set_spec[set][si];
-            E.ip[(((long)n * E.n_specs + sidx) * Kc + gch[gi]) * E.T_total + t0] = v[gi * I + si];
-          }
-    }
+    aux_products<W, MAXC, SMALL>(E, c, R, n, set, t0, psip, lamc);
     }  // doB
     if (n == 0) break;
     if (!doA) {
@@ -844,6 +860,54 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
   cl_sync();
 }
 
+template <int W, int MAXC, bool SMALL, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 : 1)
+    lg_k_cl_backward(const __grid_constant__ LgEngineArgs E) {
+  cl_backward_body<W, MAXC, SMALL, SPLIT, false>(E);
+}
+template <int W, int MAXC, bool SMALL>
+__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_adjoint(const __grid_constant__ LgEngineArgs E) {
+  cl_backward_body<W, MAXC, SMALL, false, true>(E);
+}
+// Derivative products as independent items (step n, trajectory group g), item = k * n_groups + g
+// with k = N - 1 - n, dealt round-robin to the grid's co-resident clusters; psi_{n-1} and
+// lambda_s(n) read from the adjoint sweep's store.
+template <int W, int MAXC, bool SMALL>
+__global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_aux(const __grid_constant__ LgEngineArgs E) {
+  const int cid = blockIdx.x / (int)cl_size(), ncl = gridDim.x / (int)cl_size();
+  const int Kc = E.Kc, N = E.N;
+  const int cst = 1 + E.cta_Imax, cmax = (Kc + 1) > cst ? (Kc + 1) : cst;
+  Cl c = make_cl(E, cmax, cst, W, false);
+  ClRegs<W, MAXC, SMALL> R;
+  load_cols<W, MAXC, SMALL>(E, c, R);
+  for (int q = threadIdx.x; q < c.tb0 + (c.Q > 1 ? 4 : 2) * cmax * c.WIN; q += blockDim.x)
+    cl_sm[q] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    mb_init(cl_mb(c, 0), 1);
+    mb_init(cl_mb(c, 1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (c.acs >= 0)
+    for (int kw = 0; kw < Kc * E.Wc; ++kw) {
+      cl_sm[c.acs + kw * c.T + c.li] = c.ex ? E.Ac[(long)kw * c.d + c.orig] : make_double2(0.0, 0.0);
+      reinterpret_cast<int*>(cl_sm + c.accs)[kw * c.T + c.li] =
+          c.ex ? E.cl_accols[(long)kw * c.d + c.gi] - c.g0 + c.HW : c.H + c.li;
+    }
+  cl_sync();
+  const long items = (long)E.n_groups * N;
+  for (long it = cid; it < items; it += ncl) {
+    const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
+    const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
+    load_row<W, MAXC, SMALL>(E, c, n, R);
+    const double2 psip = c.own ? E.bk_psi[((long)g * N + n) * c.d + c.gi] : make_double2(0.0, 0.0);
+    double2 lamc[LG_MAX_SPECS];
+    for (int si = 0; si < LG_MAX_SPECS; ++si)
+      lamc[si] = c.own && si < I ? E.bk_lam[(((long)g * N + n) * E.cta_Imax + si) * c.d + c.gi] : make_double2(0.0, 0.0);
+    aux_products<W, MAXC, SMALL>(E, c, R, n, set, t0, psip, lamc);
+  }
+  cl_sync();
+}
+
 #include "lg_sweep_cl_large.cuh"
 
 // Instantiations for one ELL width per translation unit (lg_sweep_cl_w*.cu), so the
@@ -856,15 +920,18 @@ __global__ void __launch_bounds__(SPLIT ? 192 : (SMALL ? 256 : 640), SPLIT ? 2 :
     }                                                                                                    \
     return nullptr;                                                                                      \
   }
-// backward: 0 forward, 1 backward, 3 forward line-search batch; LARGE only: 4 adjoint sweep storing
-// psi_{n-1} / lambda_s(n), 5 derivative-product items
+// backward: 0 forward, 1 backward, 3 forward line-search batch, 4 adjoint sweep storing psi_{n-1} /
+// lambda_s(n), 5 derivative-product items (two-phase backward)
 #define LG_CL_CASE(W_, C_)                                                                                   \
   case C_ * 2:                                                                                               \
     if (backward == 3) return (void*)lg_k_cl_forward_batch<W_, C_, false>;                                  \
-    if (backward >= 4) return nullptr;                                                                       \
+    if (backward == 4) return (void*)lg_k_cl_adjoint<W_, C_, false>;                                        \
+    if (backward == 5) return (void*)lg_k_cl_aux<W_, C_, false>;                                            \
     return backward ? (void*)lg_k_cl_backward<W_, C_, false> : (void*)lg_k_cl_forward<W_, C_, false>;        \
   case C_ * 2 + 1:                                                                                           \
     if (small == 2) return backward == 1 ? (void*)lg_k_cl_backward<W_, C_, true, true> : nullptr;            \
+    if (backward == 4 && small == 1) return (void*)lg_k_cl_adjoint<W_, C_, true>;                            \
+    if (backward == 5 && small == 1) return (void*)lg_k_cl_aux<W_, C_, true>;                                \
     if (backward >= 4 && small != 3) return nullptr;                                                         \
     if (small == 3)                                                                                          \
       return backward == 3 ? (void*)lg_k_cll_forward_batch<W_, C_, 2>                                        \

@@ -232,14 +232,18 @@ def test_c5_prefix_dense_dmma():
 # ----------------------------------------------------------------------------- cluster-engine variants
 
 
-@pytest.mark.parametrize("size,q,nosmall", [(16, 1, 0), (16, 3, 0), (16, 6, 0), (8, 3, 0), (16, 3, 1), (8, 2, 1),
-                                            (16, 1, 2), (8, 1, 2)])
-def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
+@pytest.mark.parametrize("size,q,nosmall,fused", [(16, 1, 0, 0), (16, 3, 0, 0), (16, 6, 0, 0), (8, 3, 0, 0),
+                                                  (16, 3, 1, 0), (8, 2, 1, 0), (16, 1, 2, 0), (8, 1, 2, 0),
+                                                  (16, 3, 0, 1), (8, 3, 0, 1), (16, 3, 1, 1), (16, 1, 2, 1)])
+def test_cluster_engine_variants(size, q, nosmall, fused, monkeypatch):
     """Every cluster-engine layout (cluster size, ghost-zone block length Q, SMALL, generic or
-    LARGE (three rows per thread, nosmall == 2) kernels) against the golden c3 prefix and the
-    plan-sensitive block-aux stress variant."""
+    LARGE (two rows per thread, nosmall == 2) kernels), with the two-phase backward (adjoint sweep
+    + derivative-product items, the default) and the fused one (split backward for the SMALL
+    kernels) against the golden c3 prefix and the plan-sensitive block-aux stress variant."""
     monkeypatch.setenv("LG_CL_SIZE", str(size))
     monkeypatch.setenv("LG_CL_Q", str(q))
+    if fused:
+        monkeypatch.setenv("LG_CL_FUSED", "1")
     if nosmall == 1:
         monkeypatch.setenv("LG_CL_NOSMALL", "1")
     if nosmall == 2:
@@ -254,6 +258,7 @@ def test_cluster_engine_variants(size, q, nosmall, monkeypatch):
         _check(npb.grad(a), z["cost"], z["grad"])
         assert abs(npb.cost(a) - float(z["cost"])) <= COST_TOL
     assert npb.engine.startswith("cluster-large" if nosmall == 2 else "cluster"), npb.engine
+    assert ("adjoint" in npb.engine) == (not fused), npb.engine
     zs = G.sub(G.load("stress"), "s_block160")
     hs, hc = G.mats(zs)
     om = G.penalty(zs)
