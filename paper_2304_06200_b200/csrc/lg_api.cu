@@ -102,7 +102,8 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     bsm = p->ws_bwd_smem;
     bblock = dim3(p->ws_bwd_threads);
   }
-  auto cl_launch = [&](void* f, bool backward, int clusters = 0, bool allow_split = true) -> int {
+  auto cl_launch = [&](void* f, bool backward, int clusters = 0, bool allow_split = true,
+                       cudaStream_t st = nullptr) -> int {
     E.cl_acs = backward ? p->cl_acs : 0;
     const bool split = backward && p->cl_split && allow_split;
     E.cl_R = split ? p->cl_R_b : p->cl_R;
@@ -113,7 +114,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
     cfg.gridDim = dim3((clusters ? clusters : p->n_groups) * p->cl_CS);
     cfg.blockDim = dim3(split ? p->cl_T_b : p->threads);
     cfg.dynamicSmemBytes = split ? p->cl_smem_split : (backward ? p->cl_smem_b : p->cl_smem);
-    cfg.stream = p->stream;
+    cfg.stream = st ? st : p->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = p->cl_CS;
@@ -154,6 +155,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
           p->bk_cap = 0;
           p->d_bk_psi = p->bkmem.alloc<double2>((size_t)need);
           p->d_bk_lam = p->bkmem.alloc<double2>((size_t)need * std::max(p->cta_Imax, 1));
+          p->d_bk_flag = p->bkmem.alloc<unsigned>((size_t)p->n_groups * p->cl_CS + 2);  // + counter, error
           if (p->bkmem.failed) {
             p->bkmem.release();
           } else {
@@ -163,12 +165,42 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
         two = p->bk_cap >= need;
       }
       if (two) {
+        // adjoint sweep (n_groups clusters) and derivative-product items; when every adjoint cluster
+        // and at least one item cluster fit on the GPU at once, a first item kernel runs on the spare
+        // clusters CONCURRENTLY (second stream; items wait on the adjoint's per-step flags; sized so
+        // both kernels are co-resident, so the waits cannot starve the adjoint), and a second one
+        // takes the adjoint's clusters when it ends.  Both pull items from one atomic counter.
         E.bk_psi = p->d_bk_psi;
         E.bk_lam = p->d_bk_lam;
-        rc = cl_launch(lg_cl_kernel(4, p->W, p->cl_maxc, p->cl_small), true, 0, false);
+        E.bk_flag = p->d_bk_flag;
+        E.bk_next = p->d_bk_flag + (long)p->n_groups * p->cl_CS;
+        CK(cudaMemsetAsync(p->d_bk_flag, 0, sizeof(unsigned) * ((size_t)p->n_groups * p->cl_CS + 2), p->stream));
+        const long items = (long)p->n_groups * N;
+        const int spare = p->cl_aux_ncl - p->n_groups;
+        const bool conc = spare >= 1 && !std::getenv("LG_CL_SERIAL");
+        void* fa = lg_cl_kernel(4, p->W, p->cl_maxc, p->cl_small);
+        void* fi = lg_cl_kernel(5, p->W, p->cl_maxc, p->cl_small);
+        if (conc) {
+          if (!p->stream2) CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+          if (!p->ev_fork) CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+          if (!p->ev_join) CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+          CK(cudaEventRecord(p->ev_fork, p->stream));
+          CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
+          rc = cl_launch(fi, true, (int)std::min<long>(spare, items), false, p->stream2);
+          if (rc) return rc;
+        }
+        rc = cl_launch(fa, true, 0, false);
         if (rc) return rc;
-        rc = cl_launch(lg_cl_kernel(5, p->W, p->cl_maxc, p->cl_small), true,
-                       (int)std::min<long>(p->cl_aux_ncl, (long)p->n_groups * N), false);
+        rc = cl_launch(fi, true, (int)std::min<long>(conc ? p->n_groups : p->cl_aux_ncl, items), false);
+        if (rc) return rc;
+        if (conc) {
+          CK(cudaEventRecord(p->ev_join, p->stream2));
+          CK(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
+        }
+        unsigned werr = 0;  // item-kernel watchdog (lg_sweep_cl.cuh bk_wait)
+        CK(cudaMemcpyAsync(&werr, E.bk_next + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        if (werr) return fail(LG_CUDA_ERROR, "two-phase backward: derivative items timed out waiting on the adjoint sweep");
       } else {
         rc = cl_launch(bwd, true);
       }

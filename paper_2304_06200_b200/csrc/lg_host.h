@@ -164,6 +164,9 @@ struct lg_problem {
   DevMem bkmem;        // ... its psi_{n-1} / lambda_s(n) store
   long bk_cap = 0;
   double2 *d_bk_psi = nullptr, *d_bk_lam = nullptr;
+  unsigned* d_bk_flag = nullptr;  // [n_groups][CS] steps stored, then [1] item counter
+  cudaStream_t stream2 = nullptr;  // concurrent derivative-product items (two-phase backward)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int *d_cl_perm = nullptr, *d_cl_inv = nullptr, *d_cl_cols = nullptr, *d_cl_accols = nullptr;
   unsigned char* d_cl_slot = nullptr;
   int n_groups = 0, n_slabs = 1, threads = 512, smem_mode = 0, smem_bytes = 0, red_cap = 64;
@@ -249,6 +252,9 @@ struct lg_problem {
     bkmem.release();
     mem.release();
     if (d_splitws) cudaFree(d_splitws);
+    if (stream2) cudaStreamDestroy(stream2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
   void mark(int i) {

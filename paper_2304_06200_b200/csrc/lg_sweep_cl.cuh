@@ -111,6 +111,34 @@ __device__ __forceinline__ unsigned cl_size() {
   return r;
 }
 
+// Two-phase backward hand-off.  The adjoint sweep publishes, per (group, cluster rank), how many
+// steps it has stored (after a CTA barrier, one release store at gpu scope: cumulative over the
+// CTA's stores); an item CTA waits for its own rank's count with an acquire load.  Items come from
+// an atomic counter (rank 0 fetches, every rank of the cluster gets the index through DSMEM).
+__device__ __forceinline__ void bk_publish(const LgEngineArgs& E, int g, unsigned rank, unsigned cs, unsigned steps) {
+  __syncthreads();
+  if (threadIdx.x == 0)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(E.bk_flag + (long)g * cs + rank), "r"(steps) : "memory");
+}
+// (watchdog: a wait longer than ~20 s -- the adjoint sweep can no longer be running -- gives up and
+// raises the error word after the item counter, which the host turns into LG_CUDA_ERROR; it never hangs)
+__device__ __forceinline__ void bk_wait(const LgEngineArgs& E, int g, unsigned rank, unsigned cs, unsigned steps) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    const long long t0 = clock64();
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(E.bk_flag + (long)g * cs + rank) : "memory");
+      if (v >= steps) break;
+      if (clock64() - t0 > 40000000000LL) {
+        atomicExch(E.bk_next + 1, 1u);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 // Per-CTA context.  Thread li handles renumbered row gi = g0 - E + li (window
 // position li + H); own rows are li in [E, E + R).
 struct Cl {
@@ -782,9 +810,12 @@ __device__ __forceinline__ void cl_backward_body(const LgEngineArgs& E) {
 #pragma unroll
       for (int q = 1; q < MAXC; ++q)
         if (q - 1 < LG_MAX_SPECS) lamn[q - 1] = R.cur[q];
-      if (STORE && c.own) {  // hand psi_{n-1} and lambda_s(n) to the item kernel
-        E.bk_psi[((long)g * N + n) * c.d + c.gi] = psip;
-        for (int si = 0; si < I; ++si) E.bk_lam[(((long)g * N + n) * E.cta_Imax + si) * c.d + c.gi] = lam[si];
+      if (STORE) {  // hand psi_{n-1} and lambda_s(n) to the item kernel
+        if (c.own) {
+          E.bk_psi[((long)g * N + n) * c.d + c.gi] = psip;
+          for (int si = 0; si < I; ++si) E.bk_lam[(((long)g * N + n) * E.cta_Imax + si) * c.d + c.gi] = lam[si];
+        }
+        bk_publish(E, g, (unsigned)(c.base + c.rank), cl_size(), (unsigned)(N - n));
       }
       if (SPLIT) {  // hand psi_{n-1} and lambda_s(n) to the partner CTA of group 1
         if (it >= LG_CL_HR) mb_wait_cluster(cl_mb(c, 3 + LG_CL_HR + hs), (unsigned)((it / LG_CL_HR) - 1) & 1u);
@@ -894,10 +925,23 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_aux(const __grid
           c.ex ? E.cl_accols[(long)kw * c.d + c.gi] - c.g0 + c.HW : c.H + c.li;
     }
   cl_sync();
+  (void)cid;
+  (void)ncl;
   const long items = (long)E.n_groups * N;
-  for (long it = cid; it < items; it += ncl) {
+  unsigned* slot = reinterpret_cast<unsigned*>(cl_sm + c.rt + 64) + 24;  // fetched item index (after the channel table)
+  for (;;) {
+    if (c.rank == 0 && threadIdx.x == 0) {
+      const unsigned it = atomicAdd(E.bk_next, 1u);
+      for (int r = 0; r < c.CS; ++r)
+        asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cl_map(slot, r)), "r"(it) : "memory");
+    }
+    cl_sync();
+    const long it = *slot;
+    cl_sync();  // every rank has read the index before rank 0 may overwrite it
+    if (it >= items) break;
     const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
     const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
+    bk_wait(E, g, (unsigned)c.rank, (unsigned)c.CS, (unsigned)(N - n));
     load_row<W, MAXC, SMALL>(E, c, n, R);
     const double2 psip = c.own ? E.bk_psi[((long)g * N + n) * c.d + c.gi] : make_double2(0.0, 0.0);
     double2 lamc[LG_MAX_SPECS];

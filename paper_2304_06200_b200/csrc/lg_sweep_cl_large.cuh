@@ -586,6 +586,7 @@ __device__ __forceinline__ void cll_backward_body(const LgEngineArgs& E) {
           bp[c.gi(r)] = psip[r];
           for (int si = 0; si < I; ++si) bl[(long)si * c.d + c.gi(r)] = lam[r][si];
         }
+      bk_publish(E, g, (unsigned)c.rank, (unsigned)c.CS, (unsigned)(N - n));
     } else {
       aux_products_l(E, c, R, n, set, t0, psip, lam);
     }
@@ -651,10 +652,23 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_aux(const __grid_const
   ClL c = make_cll<RPT>(E, cmax, true);
   ClLRegs<W, MAXC, RPT> R;
   cll_backward_setup(E, c, R);
+  (void)cid;
+  (void)ncl;
   const long items = (long)E.n_groups * N;
-  for (long it = cid; it < items; it += ncl) {
+  unsigned* slot = reinterpret_cast<unsigned*>(cl_sm + c.rt + 64) + 24;  // fetched item index (after the channel table)
+  for (;;) {
+    if (c.rank == 0 && threadIdx.x == 0) {
+      const unsigned it = atomicAdd(E.bk_next, 1u);
+      for (int r = 0; r < c.CS; ++r)
+        asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cl_map(slot, r)), "r"(it) : "memory");
+    }
+    cl_sync();
+    const long it = *slot;
+    cl_sync();  // every rank has read the index before rank 0 may overwrite it
+    if (it >= items) break;
     const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
     const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
+    bk_wait(E, g, (unsigned)c.rank, (unsigned)c.CS, (unsigned)(N - n));
     load_row_l(E, c, n, R);
     const double2* bp = E.bk_psi + ((long)g * N + n) * c.d;
     const double2* bl = E.bk_lam + ((long)g * N + n) * E.cta_Imax * c.d;
