@@ -82,7 +82,7 @@ typedef struct {
   int64_t shard_begin, shard_end;
   /* Backend (src/derivatives.py:48-51): 0 SCALING_SQUARING (certified Taylor action),
    * 1 DIAGONALIZATION (per-step eigenfactorisation, src/derivatives.py:228-275; dense
-   * operators, d <= 128). */
+   * operators: the CTA engine applies the propagators for d <= 128, the dense GEMM engine above). */
   int32_t backend;
 } lg_problem_desc;
 

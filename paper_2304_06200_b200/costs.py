@@ -6,7 +6,7 @@ Same names, argument meaning and error behaviour as ``leangrape.costs``:
 ``c1/c3_gate_grad``, ``forward_propagate``.  Every evaluation runs the
 sm_100a kernels through the C ABI (include/leangrape_b200.h); there is no CPU
 fallback.  Both backends run on the device: SCALING_SQUARING (the certified
-Taylor action) and DIAGONALIZATION (per-step eigenfactorisation, dense d <= 128,
+Taylor action) and DIAGONALIZATION (per-step eigenfactorisation on the device, dense operators,
 lg_diag.cu).
 
 K-state block extension (documented in DESIGN.md):

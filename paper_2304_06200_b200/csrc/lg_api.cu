@@ -419,7 +419,7 @@ const char* lg_engine_name(lg_problem* p) {
     case 0: return "grid:lg_k_backward";
     case 1: return "grid-multi:lg_k_backward";
     case 2: return "cta:lg_k_cta_backward";
-    case 3: return "dense:lg_k_zgemm_taylor";
+    case 3: return p->backend == 1 ? "dense-diag:lg_k_zgemm_taylor" : "dense:lg_k_zgemm_taylor";
     case 4: return p->ws_cluster ? "ws-cluster:lg_k_wsc_backward" : "ws:lg_k_ws_backward";
     case 5: {
       const bool two = p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");

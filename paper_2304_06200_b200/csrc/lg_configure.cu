@@ -587,7 +587,7 @@ bool configure_cta(lg_problem* p, int nsm, int smem_optin) {
 
 // Choose the work decomposition and the shared-memory placement.
 int configure(lg_problem* p) {
-  if (p->dense_large) return configure_dense(p);
+  if (p->dense_large || p->diag_dense) return configure_dense(p);
   int dev = p->device, nsm = 0, smem_optin = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));

@@ -60,6 +60,12 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
                 p->stream);
 }
 
+// Y <- Op X over C columns: one GEMM, no Taylor recursion (DIAGONALIZATION backend: Op = U_n,
+// U_n^dagger or dU_n/da_k as formed by prepare_diag, column-major d x d)
+int dense_apply(lg_problem* p, const double2* op, int C, const double2* X, double2* Y) {
+  return dense_gemm(p, op, X, nullptr, nullptr, C, 1.0, true, true, nullptr, Y, p->dd_tb0);
+}
+
 // cur <- (T_m(sgn A / s))^s x over C columns (columns contiguous, stride d)
 int dense_chain(lg_problem* p, int C, double sgn, int m, int s, const double2* x, double2* cur) {
   const double2* prev = x;
@@ -227,7 +233,9 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
   std::vector<int4> pl((size_t)N * (Kc + 1));
   CK(cudaMemcpyAsync(pl.data(), p->d_plan, sizeof(int4) * pl.size(), cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
-  if (!(p->dense_dt == dt)) {
+  const bool diag = p->backend == 1;  // propagators formed by prepare_diag (lg_diag.cu)
+  const long dd = d * d;
+  if (!diag && !(p->dense_dt == dt)) {
     for (int c = 0; c < Kc; ++c) {
       double2** none = nullptr;
       rc = dense_form(p, p->d_hc_dense_host[c], none, nullptr, 0, dt, p->d_Acd[c]);
@@ -270,9 +278,13 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
     // ---- forward sweep
     for (long n = 0; n < N; ++n) {
       const int4 q = pl[(size_t)n * (Kc + 1)];
-      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
-      if (rc) return rc;
-      rc = dense_chain(p, T, 1.0, q.x, q.y, p->dd_st, p->dd_cur);
+      if (diag) {
+        rc = dense_apply(p, p->d_A + n * dd, T, p->dd_st, p->dd_cur);
+      } else {
+        rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
+        if (rc) return rc;
+        rc = dense_chain(p, T, 1.0, q.x, q.y, p->dd_st, p->dd_cur);
+      }
       if (rc) return rc;
       CK(cudaMemcpyAsync(p->dd_st, p->dd_cur, sizeof(double2) * T * d, cudaMemcpyDeviceToDevice, p->stream));
       const bool fin_step = n == N - 1;
@@ -371,13 +383,30 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
     int gch[LG_MAX_CHANNELS];
     for (long n = N - 1; n >= 0; --n) {
       const int4* pn = &pl[(size_t)n * (Kc + 1)];
-      rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
-      if (rc) return rc;
       const int cadj = n > 0 ? T * (1 + I) : T;
-      rc = dense_chain(p, cadj, -1.0, pn[0].x, pn[0].y, p->dd_st, p->dd_nx);
+      if (diag) {
+        rc = dense_apply(p, p->d_Ud + n * dd, cadj, p->dd_st, p->dd_nx);
+      } else {
+        rc = dense_form(p, p->d_hs_dense, p->d_hc_dense_ptrs, p->d_amps + n * Kc, Kc, dt, p->d_Ad);
+        if (rc) return rc;
+        rc = dense_chain(p, cadj, -1.0, pn[0].x, pn[0].y, p->dd_st, p->dd_nx);
+      }
       if (rc) return rc;
       unsigned done = 0;
-      for (int kc = 0; kc < Kc; ++kc) {
+      for (int kc = 0; kc < Kc && diag; ++kc) {  // <lambda_s(n)| dU_n/da_k psi_{n-1}>, one GEMM per channel
+        rc = dense_apply(p, p->d_D + (n * Kc + kc) * dd, T, p->dd_nx, p->dd_xcur);
+        if (rc) return rc;
+        std::vector<std::pair<const double2*, const double2*>> pr;
+        std::vector<DotOut> to;
+        for (int si = 0; si < I; ++si)
+          for (int t = 0; t < T; ++t) {
+            pr.push_back({lam(p->dd_st, si, t), p->dd_xcur + (long)t * d});
+            to.push_back({p->d_ip + (((long)n * S + sp_idx[si]) * Kc + kc) * Tt + t0 + t, 0});
+          }
+        rc = dense_dots(p, pr, to);
+        if (rc) return rc;
+      }
+      for (int kc = 0; kc < Kc && !diag; ++kc) {
         if (done & (1u << kc)) continue;
         int G = 0;
         for (int k2 = kc; k2 < Kc; ++k2)

@@ -446,6 +446,9 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
   // (tests exercise its kernels against the dense goldens below d = 512)
   const char* fe = std::getenv("LG_ENGINE");
   p->dense_large = p->dense && D->backend == 0 && (d > 512 || (fe && std::string(fe) == "dense"));
+  // DIAGONALIZATION above the CTA engine's d <= 128 (or LG_ENGINE=dense): the propagators
+  // U_n, U_n^dagger, dU_n/da_k are applied by the dense GEMM engine, one GEMM per application
+  p->diag_dense = p->dense && D->backend == 1 && (d > 128 || (fe && std::string(fe) == "dense"));
   // ---- terms and trajectory sets
   if (D->n_terms > LG_MAX_SPECS) return fail(LG_UNSUPPORTED, "more than 8 cost terms");
   bool has_state = false, has_gate = false;
@@ -499,8 +502,8 @@ int build_problem(const lg_problem_desc* D, lg_problem* p) {
   // sharding (multi-GPU): each set propagates only trajectories [shard_begin, shard_end) of itself
   p->backend = D->backend;
   if (p->backend < 0 || p->backend > 1) return fail(LG_INVALID_ARG, "unknown backend");
-  if (p->backend == 1 && (!p->dense || d > 128))
-    return fail(LG_UNSUPPORTED, "the DIAGONALIZATION backend runs dense operators with d <= 128 on the device");
+  if (p->backend == 1 && !p->dense)
+    return fail(LG_UNSUPPORTED, "the DIAGONALIZATION backend runs dense operators on the device");
   p->shard_b = D->shard_end > 0 ? D->shard_begin : 0;
   p->shard_e = D->shard_end > 0 ? D->shard_end : (1L << 40);
   for (int t = 0; t < D->n_terms; ++t) {

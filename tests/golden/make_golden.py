@@ -474,10 +474,12 @@ def golden_stress():
     save("stress", **out)
 
 
-def golden_diag():
+def golden_diag(big=False):
     """The reference's DIAGONALIZATION backend (src/derivatives.py:228-275): every cost kind on a
     dense d = 40 problem (c1's model), a CSR d = 24 and a CSR d = 60 problem, random states,
-    large amplitudes.  Sparse inputs stay CSR here: the reference densifies each step."""
+    large amplitudes.  Sparse inputs stay CSR here: the reference densifies each step.
+    big=True (``diag_big``): a CSR d = 180 problem (transmon 6 x cavity 30) and a dense d = 256
+    one, above the device CTA engine's d <= 128 (the dense GEMM engine applies the propagators)."""
     out = {}
     rng = np.random.default_rng(7171)
     DIAG = derivatives.Backend.DIAGONALIZATION
@@ -511,6 +513,13 @@ def golden_diag():
             cost_state=cs, grad_state=gs, cost_state_only=css, cost_g1=cg1, grad_g1=gg1, cost_g3=cg3,
             grad_g3=gg3).items()})
 
+    if big:
+        h_s, hx, hy = tc_ops(6, 30)
+        one("d_csr180", h_s, [hx, hy], 10, 0.5, 0.5, 2, 404)
+        h_s, hx, _ = tc_ops(4, 64)
+        one("d_dense256", sparse.DenseMatrix(h_s.to_dense()), [sparse.DenseMatrix(hx.to_dense())], 8, 0.5, 0.5, 2, 405)
+        save("diag_big", **out)
+        return
     h_s, hx, _ = tc_ops(4, 10)
     one("d_dense40", sparse.DenseMatrix(h_s.to_dense()), [sparse.DenseMatrix(hx.to_dense())], 40, 0.5, 1.0, 2, 401)
     h_s, hx, hy = tc_ops(3, 8)
@@ -518,6 +527,10 @@ def golden_diag():
     h_s, hx, hy = tc_ops(3, 20)
     one("d_csr60", h_s, [hx, hy], 16, 0.25, 1.0, 2, 403)
     save("diag", **out)
+
+
+def golden_diag_big():
+    golden_diag(big=True)
 
 
 def golden_full_basis_check():

@@ -23,9 +23,17 @@ def _check(res, cost, grad):
     assert G.grad_rel(res.grad, grad) <= GRAD_TOL, G.grad_rel(res.grad, grad)
 
 
-@pytest.mark.parametrize("tag", ["d_dense40", "d_csr24", "d_csr60"])
-def test_diagonalization_backend_matches_reference(tag):
-    z = G.sub(G.load("diag"), tag)
+@pytest.mark.parametrize("golden,tag,engine", [("diag", "d_dense40", "cta"), ("diag", "d_csr24", "cta"),
+                                                ("diag", "d_csr60", "cta"), ("diag", "d_dense40", "dense-diag"),
+                                                ("diag", "d_csr60", "dense-diag"),
+                                                ("diag_big", "d_csr180", "dense-diag"),
+                                                ("diag_big", "d_dense256", "dense-diag")])
+def test_diagonalization_backend_matches_reference(golden, tag, engine, monkeypatch):
+    """d <= 128: the CTA engine (one dense operator application per propagator); above (and with
+    LG_ENGINE=dense below): the dense GEMM engine, one DMMA GEMM per propagator application."""
+    if engine == "dense-diag":
+        monkeypatch.setenv("LG_ENGINE", "dense")
+    z = G.sub(G.load(golden), tag)
     hs, hc = G.mats(z)
     om = G.penalty(z)
     N, Kc = z["amps"].shape
@@ -37,7 +45,7 @@ def test_diagonalization_backend_matches_reference(tag):
              CostTerm(CostKind.STATE_RUNNING_INFIDELITY, 0.4, target_state=z["targets"])]
     npb = NativeProblem(prob, terms, initial_states=z["psi0"])
     _check(npb.grad(a), z["cost_state"], z["grad_state"])
-    assert npb.engine.startswith("cta"), npb.engine
+    assert npb.engine.startswith(engine), npb.engine
     assert abs(npb.cost(a) - float(z["cost_state_only"])) <= COST_TOL
     for kind, ck, gk in [(CostKind.GATE_INFIDELITY, "cost_g1", "grad_g1"),
                          (CostKind.GATE_RUNNING_INFIDELITY, "cost_g3", "grad_g3")]:
@@ -45,15 +53,17 @@ def test_diagonalization_backend_matches_reference(tag):
         _check(NativeProblem(prob, t, basis=z["basis"]).grad(a), z[ck], z[gk])
 
 
-def test_diagonalization_backend_limits():
-    """Sparse problems above d = 128 are refused (the Taylor path handles them), not run on the host."""
+def test_diagonalization_backend_sparse_input_is_densified():
+    """Sparse operators with the DIAGONALIZATION backend are densified (the reference densifies
+    each step, src/derivatives.py:228-246) and above d = 128 run on the dense GEMM engine."""
+    import numpy as np
+
     from paper_2304_06200_b200 import models
 
     h_s, hx, hy = models.transmon_cavity_ops(6, 30)  # d = 180
     prob = ControlProblem(h_s, (hx, hy), backend=Backend.DIAGONALIZATION)
-    import numpy as np
-
     t = [CostTerm(CostKind.GATE_INFIDELITY, 1.0, target_images=np.eye(180, dtype=np.complex128)[:2])]
-    with pytest.raises(NotImplementedError):
-        NativeProblem(prob, t, basis=np.eye(180, dtype=np.complex128)[:2]).grad(
-            ControlField(3, 2, 0.5, np.zeros((3, 2))))
+    npb = NativeProblem(prob, t, basis=np.eye(180, dtype=np.complex128)[:2])
+    assert npb.engine.startswith("dense-diag"), npb.engine
+    res = npb.grad(ControlField(3, 2, 0.5, np.zeros((3, 2))))
+    assert np.isfinite(res.cost) and np.all(np.isfinite(res.grad))

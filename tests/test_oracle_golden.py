@@ -116,10 +116,11 @@ def test_stress_cost_grad(tag):
         assert G.grad_rel(grad, z[gk]) <= 1e-12
 
 
-@pytest.mark.parametrize("tag", ["d_dense40", "d_csr24", "d_csr60"])
-def test_diagonalization_backend_cost_grad(tag):
+@pytest.mark.parametrize("golden,tag", [("diag", "d_dense40"), ("diag", "d_csr24"), ("diag", "d_csr60"),
+                                        ("diag_big", "d_csr180"), ("diag_big", "d_dense256")])
+def test_diagonalization_backend_cost_grad(golden, tag):
     """The oracle's DIAGONALIZATION restatement against the reference's own backend."""
-    z = G.sub(G.load("diag"), tag)
+    z = G.sub(G.load(golden), tag)
     hs, hc = G.mats(z, "oracle")
     om = G.penalty(z, "oracle")
     p = O.Problem(hs, tuple(hc), initial_states=z["psi0"], basis=z["basis"], backend="diagonalization")
