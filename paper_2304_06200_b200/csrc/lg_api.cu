@@ -155,7 +155,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
           p->bk_cap = 0;
           p->d_bk_psi = p->bkmem.alloc<double2>((size_t)need);
           p->d_bk_lam = p->bkmem.alloc<double2>((size_t)need * std::max(p->cta_Imax, 1));
-          p->d_bk_flag = p->bkmem.alloc<unsigned>((size_t)p->n_groups * p->cl_CS + 2);  // + counter, error
+          p->d_bk_flag = p->bkmem.alloc<unsigned>((size_t)p->n_groups * p->cl_CS + 3);  // + counter, error, started
           if (p->bkmem.failed) {
             p->bkmem.release();
           } else {
@@ -174,24 +174,59 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
         E.bk_lam = p->d_bk_lam;
         E.bk_flag = p->d_bk_flag;
         E.bk_next = p->d_bk_flag + (long)p->n_groups * p->cl_CS;
-        CK(cudaMemsetAsync(p->d_bk_flag, 0, sizeof(unsigned) * ((size_t)p->n_groups * p->cl_CS + 2), p->stream));
+        E.bk_ranks = p->cl_CS;
+        E.bk_conc = 0;
+        CK(cudaMemsetAsync(p->d_bk_flag, 0, sizeof(unsigned) * ((size_t)p->n_groups * p->cl_CS + 3), p->stream));
         const long items = (long)p->n_groups * N;
-        const int spare = p->cl_aux_ncl - p->n_groups;
-        const bool conc = spare >= 1 && !std::getenv("LG_CL_SERIAL");
+        const bool ilay = p->cli_CS > 0;  // items on their own (LARGE, smaller-cluster) layout
+        const int incl = ilay ? p->cli_ncl : p->cl_aux_ncl;
         void* fa = lg_cl_kernel(4, p->W, p->cl_maxc, p->cl_small);
-        void* fi = lg_cl_kernel(5, p->W, p->cl_maxc, p->cl_small);
+        void* fi = lg_cl_kernel(5, p->W, p->cl_maxc, ilay ? 3 : p->cl_small);
+        auto item_launch = [&](int clusters, cudaStream_t st) -> int {
+          if (!ilay) return cl_launch(fi, true, clusters, false, st);
+          LgEngineArgs Ei = E;
+          Ei.cl_acs = 1;
+          Ei.cl_R = p->cli_R;
+          Ei.cl_Q = 1;
+          Ei.cl_E = 0;
+          void* iargs[] = {&Ei};
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(clusters * p->cli_CS);
+          cfg.blockDim = dim3(320);
+          cfg.dynamicSmemBytes = p->cli_smem;
+          cfg.stream = st ? st : p->stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = p->cli_CS;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          ++g_launches;
+          ensure_smem(fi, cfg.dynamicSmemBytes);
+          cudaError_t e = cudaLaunchKernelExC(&cfg, fi, iargs);
+          if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("item launch: ") + cudaGetErrorString(e));
+          return LG_OK;
+        };
+        // concurrent item kernel: only when the adjoint sweep fits the GPU at once (its clusters then
+        // all start; the item kernel checks that and otherwise exits at once, lg_sweep_cl.cuh bk_may_run)
+        const bool conc = p->n_groups < p->cl_aux_ncl && !std::getenv("LG_CL_SERIAL");
         if (conc) {
           if (!p->stream2) CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
           if (!p->ev_fork) CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
           if (!p->ev_join) CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
           CK(cudaEventRecord(p->ev_fork, p->stream));
-          CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
-          rc = cl_launch(fi, true, (int)std::min<long>(spare, items), false, p->stream2);
-          if (rc) return rc;
         }
         rc = cl_launch(fa, true, 0, false);
         if (rc) return rc;
-        rc = cl_launch(fi, true, (int)std::min<long>(conc ? p->n_groups : p->cl_aux_ncl, items), false);
+        if (conc) {
+          CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
+          E.bk_conc = 1;
+          rc = item_launch((int)std::min<long>(incl, items), p->stream2);
+          E.bk_conc = 0;
+          if (rc) return rc;
+        }
+        rc = item_launch((int)std::min<long>(incl, items), nullptr);
         if (rc) return rc;
         if (conc) {
           CK(cudaEventRecord(p->ev_join, p->stream2));
@@ -425,7 +460,7 @@ const char* lg_engine_name(lg_problem* p) {
       const bool two = p->cl_aux_ncl > 0 && !std::getenv("LG_CL_FUSED");
       if (p->cl_small >= 3)
         return two ? "cluster-large:lg_k_cll_adjoint+lg_k_cll_aux" : "cluster-large:lg_k_cll_backward";
-      if (two) return "cluster-2phase:lg_k_cl_adjoint+lg_k_cl_aux";
+      if (two) return p->cli_CS > 0 ? "cluster-2phase:lg_k_cl_adjoint+lg_k_cll_aux" : "cluster-2phase:lg_k_cl_adjoint+lg_k_cl_aux";
       return p->cl_split ? "cluster-split:lg_k_cl_backward" : "cluster:lg_k_cl_backward";
     }
     default: return "unknown";

@@ -366,6 +366,44 @@ bool configure_cl(lg_problem* p, int smem_optin) {
     }
     p->cl_aux_ncl = ncl;
   }
+  // Item layout.  The derivative-product items are independent, so they need not use the sweeps'
+  // cluster size (chosen for the latency of one trajectory's chain): the smallest power-of-two
+  // cluster whose CTAs fit the LARGE kernels (<= 640 rows each) gives them more rows per exchange
+  // and per CTA (c3: 2 CTAs of 600 rows instead of 16 of 75 + ghost rows).  The bk store is in
+  // renumbered rows, so any partition can read it.
+  p->cli_CS = 0;
+  if (p->cl_aux_ncl > 0 && small != 3 && p->Wc <= 2 && !std::getenv("LG_CL_NOITEMLAYOUT")) {
+    void* fi = lg_cl_kernel(5, p->W, maxc, 3);
+    for (int cs = 2; cs <= 8 && fi; cs *= 2) {
+      const int Ri = (int)((d + cs - 1) / cs), LT = 320, cstl = cmax | 1;
+      if (Ri > 2 * LT || Ri < H || 16L * cstl * (Ri + 2 * H) >= 65536) continue;
+      const int wbl = lg_cll_mb_word(Ri, H, LT, cstl, p->Kc * 2, 2) + 1;
+      if ((long)wbl * 16 > cap || cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, wbl * 16) != cudaSuccess)
+        continue;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(LT);
+      cfg.dynamicSmemBytes = wbl * 16;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, fi, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        ncl = 0;
+      }
+      if (ncl < 1) continue;
+      p->cli_CS = cs;
+      p->cli_R = Ri;
+      p->cli_smem = wbl * 16;
+      p->cli_ncl = ncl;
+      break;
+    }
+  }
   p->cl_maxc = maxc;
   p->cl_smem = words * 16;
   p->cl_smem_b = words_b * 16;

@@ -161,7 +161,9 @@ struct lg_problem {
   int cl_split = 0, cl_R_b = 0, cl_Q_b = 1, cl_E_b = 0, cl_T_b = 0, cl_smem_split = 0;  // split backward
   int cl_CS = 0, cl_R = 0, cl_H = 0, cl_Q = 1, cl_E = 0, cl_small = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
   unsigned cl_cshare = 0;  // bit k: control channel k has channel k-1's (renumbered) column pattern
-  int cl_aux_ncl = 0;  // LARGE two-phase backward: co-resident clusters of the item kernel (0: fused backward)
+  int cl_aux_ncl = 0;  // two-phase backward: co-resident clusters of the item kernel (0: fused backward)
+  // item layout: the derivative-product items on smaller clusters of the LARGE kernels (0: the sweep layout)
+  int cli_CS = 0, cli_R = 0, cli_smem = 0, cli_ncl = 0;
   DevMem bkmem;        // ... its psi_{n-1} / lambda_s(n) store
   long bk_cap = 0;
   double2 *d_bk_psi = nullptr, *d_bk_lam = nullptr;

@@ -122,12 +122,17 @@ __device__ __forceinline__ void bk_publish(const LgEngineArgs& E, int g, unsigne
 }
 // (watchdog: a wait longer than ~20 s -- the adjoint sweep can no longer be running -- gives up and
 // raises the error word after the item counter, which the host turns into LG_CUDA_ERROR; it never hangs)
-__device__ __forceinline__ void bk_wait(const LgEngineArgs& E, int g, unsigned rank, unsigned cs, unsigned steps) {
-  if (threadIdx.x == 0) {
+// An item CTA may own rows of several adjoint CTAs (the item layout can use bigger CTAs), so it
+// waits for every adjoint rank of the trajectory: thread t < bk_ranks watches rank t's flag.
+__device__ __forceinline__ void bk_wait(const LgEngineArgs& E, int g, unsigned steps) {
+  if ((int)threadIdx.x < E.bk_ranks) {
     unsigned v;
     const long long t0 = clock64();
     for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(E.bk_flag + (long)g * cs + rank) : "memory");
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n"
+                   : "=r"(v)
+                   : "l"(E.bk_flag + (long)g * E.bk_ranks + threadIdx.x)
+                   : "memory");
       if (v >= steps) break;
       if (clock64() - t0 > 40000000000LL) {
         atomicExch(E.bk_next + 1, 1u);
@@ -137,6 +142,35 @@ __device__ __forceinline__ void bk_wait(const LgEngineArgs& E, int g, unsigned r
     }
   }
   __syncthreads();
+}
+// adjoint sweep start: one count per cluster (after the cluster's first barrier)
+__device__ __forceinline__ void bk_started(const LgEngineArgs& E) {
+  if (cl_rank() == 0 && threadIdx.x == 0) atomicAdd(E.bk_next + 2, 1u);
+}
+// concurrent item kernel: run only if every adjoint cluster is already resident (so no item can wait
+// on an adjoint cluster that its own residency keeps off the GPU); otherwise free the SMs at once.
+// Rank 0 decides after a short spin and tells the other ranks through DSMEM.
+__device__ __forceinline__ bool bk_may_run(const LgEngineArgs& E, unsigned* slot) {
+  if (!E.bk_conc) return true;
+  if (cl_rank() == 0 && threadIdx.x == 0) {
+    unsigned v = 0, ok = 0;
+    const long long t0 = clock64();
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(E.bk_next + 2) : "memory");
+      if (v >= (unsigned)E.n_groups) {
+        ok = 1;
+        break;
+      }
+      if (clock64() - t0 > 200000LL) break;  // ~100 us
+      __nanosleep(128);
+    }
+    for (unsigned r = 0; r < cl_size(); ++r)
+      asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cl_map(slot, r)), "r"(ok) : "memory");
+  }
+  cl_sync();
+  const bool ok = *slot != 0;
+  cl_sync();
+  return ok;
 }
 
 // Per-CTA context.  Thread li handles renumbered row gi = g0 - E + li (window
@@ -739,6 +773,7 @@ __device__ __forceinline__ void cl_backward_body(const LgEngineArgs& E) {
           c.ex ? E.cl_accols[(long)kw * c.d + c.gi] - c.g0 + c.HW : c.H + c.li;
     }
   cl_sync();
+  if (STORE) bk_started(E);
   // state: psi (column 0) and the costates lambda_s (columns 1 + s), own rows in registers
   double2 psi = c.own ? E.psiN[(long)t0 * c.d + c.orig] : make_double2(0.0, 0.0);
   double2 lam[LG_MAX_SPECS];
@@ -929,6 +964,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_aux(const __grid
   (void)ncl;
   const long items = (long)E.n_groups * N;
   unsigned* slot = reinterpret_cast<unsigned*>(cl_sm + c.rt + 64) + 24;  // fetched item index (after the channel table)
+  if (!bk_may_run(E, slot)) return;
   for (;;) {
     if (c.rank == 0 && threadIdx.x == 0) {
       const unsigned it = atomicAdd(E.bk_next, 1u);
@@ -941,7 +977,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 640, 1) lg_k_cl_aux(const __grid
     if (it >= items) break;
     const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
     const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
-    bk_wait(E, g, (unsigned)c.rank, (unsigned)c.CS, (unsigned)(N - n));
+    bk_wait(E, g, (unsigned)(N - n));
     load_row<W, MAXC, SMALL>(E, c, n, R);
     const double2 psip = c.own ? E.bk_psi[((long)g * N + n) * c.d + c.gi] : make_double2(0.0, 0.0);
     double2 lamc[LG_MAX_SPECS];

@@ -497,6 +497,7 @@ __device__ __forceinline__ void cll_backward_body(const LgEngineArgs& E) {
   ClL c = make_cll<RPT>(E, cmax, true);
   ClLRegs<W, MAXC, RPT> R;
   cll_backward_setup(E, c, R);
+  if (STORE) bk_started(E);
   bool anypen = false, anyrun = false;
   for (int si = 0; si < I; ++si) {
     const int k = E.spec[E.set_spec[set][si]].kind;
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_aux(const __grid_const
   (void)ncl;
   const long items = (long)E.n_groups * N;
   unsigned* slot = reinterpret_cast<unsigned*>(cl_sm + c.rt + 64) + 24;  // fetched item index (after the channel table)
+  if (!bk_may_run(E, slot)) return;
   for (;;) {
     if (c.rank == 0 && threadIdx.x == 0) {
       const unsigned it = atomicAdd(E.bk_next, 1u);
@@ -668,7 +670,7 @@ __global__ void __launch_bounds__(CLL_T(RPT), 1) lg_k_cll_aux(const __grid_const
     if (it >= items) break;
     const int g = (int)(it % E.n_groups), n = N - 1 - (int)(it / E.n_groups);
     const int set = E.grp_set[g], t0 = E.grp_t0[g], I = E.set_nspec[set];
-    bk_wait(E, g, (unsigned)c.rank, (unsigned)c.CS, (unsigned)(N - n));
+    bk_wait(E, g, (unsigned)(N - n));
     load_row_l(E, c, n, R);
     const double2* bp = E.bk_psi + ((long)g * N + n) * c.d;
     const double2* bl = E.bk_lam + ((long)g * N + n) * E.cta_Imax * c.d;

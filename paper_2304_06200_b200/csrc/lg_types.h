@@ -125,7 +125,10 @@ struct LgEngineArgs {
   double2* bk_psi;          // cluster LARGE two-phase backward: psi_{n-1} [group][N][d] (renumbered rows)
   double2* bk_lam;          // ... lambda_s(n) [group][N][cta_Imax][d]
   unsigned* bk_flag;        // ... steps stored so far per (group, cluster rank) (release / acquire, gpu scope)
-  unsigned* bk_next;        // ... next derivative-product item (atomic work counter of the item kernels)
+  unsigned* bk_next;        // ... [0] next derivative-product item (atomic work counter), [1] watchdog error,
+                            //     [2] adjoint clusters started
+  int bk_ranks;             // ... cluster size of the adjoint sweep (flags per trajectory)
+  int bk_conc;              // ... this item kernel runs concurrently with the adjoint sweep
   int ws_nw;                // ws cluster backward: derivative workers per control channel
   int dense_rows;           // every operator row stores all d columns in order (dense H): slot w == column w
   const int* cl_perm;       // [d] renumbered row -> original row
