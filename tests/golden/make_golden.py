@@ -533,6 +533,29 @@ def golden_diag_big():
     golden_diag(big=True)
 
 
+BENCH_MU_CASES = [("transmon_cavity", 10, 0.1), ("transmon_cavity", 40, 0.5), ("transmon_cavity", 80, 2.0),
+                  ("three_transmons", 3, 0.1), ("three_transmons", 5, 1.0), ("qubit_chain", 3, 0.1),
+                  ("qubit_chain", 6, 0.7), ("fluxonium_pair", 6, 0.1), ("fluxonium_pair", 12, 0.05),
+                  ("zero", 4, 0.1), ("transmon_cavity", 20, 1e4)]
+
+
+def golden_bench_mu():
+    """The reference's planning sweep records (src/bench.py:169-193, measure_mu) for every model
+    family at several sizes / time steps, tau 1e-8 and 1e-14 (the latter makes large norms
+    infeasible: matvecs None -> -1 here), plus one power-law fit of a dimension sweep."""
+    from leangrape import bench as rb
+
+    rows = []
+    for tau in (1e-8, 1e-14):
+        for m, size, dt in BENCH_MU_CASES:
+            r = rb.measure_mu(m, size, dt, tau)
+            rows.append((r.d, r.norm1, r.sigma_prime, -1 if r.matvecs is None else r.matvecs, r.kappa, tau, dt, size))
+    sweep = rb.mu_vs_dim_sweep("transmon_cavity", [10, 20, 40, 80, 160], 1e-8)
+    fit = rb.fit_power_law([(r.d, r.matvecs) for r in sweep])
+    save("bench_mu", rows=np.array(rows, dtype=np.float64), models=np.array([m for _ in (0, 1) for m, _, _ in BENCH_MU_CASES]),
+         csv=np.array([r.to_csv_row() for r in sweep]), fit=np.array([fit.exponent, fit.log_prefactor, fit.r_squared]))
+
+
 def golden_full_basis_check():
     """Restated subspace gate pass == reference c1/c3_gate_grad at K == d (bitwise)."""
     rng = np.random.default_rng(31)
