@@ -57,15 +57,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
 
-    headers = [s for s in _sources() if not s.endswith(".cu")]
-    newest_header = max(os.path.getmtime(h) for h in headers)
+    def newest_dep(path, seen=None):
+        """mtime of `path` and of every local header it includes (recursively)."""
+        seen = set() if seen is None else seen
+        if path in seen or not os.path.exists(path):
+            return 0.0
+        seen.add(path)
+        t = os.path.getmtime(path)
+        with open(path) as fh:
+            for line in fh:
+                line = line.strip()
+                if line.startswith("#include \""):
+                    inc = line.split('"')[1]
+                    for base in (os.path.dirname(path), os.path.join(os.path.dirname(HERE), "include")):
+                        cand = os.path.normpath(os.path.join(base, inc))
+                        if os.path.exists(cand):
+                            t = max(t, newest_dep(cand, seen))
+                            break
+        return t
 
     def compile_unit(item):
         unit, flags = item
         obj = os.path.join(OUT, unit.replace(".cu", ".o"))
         src = os.path.join(SRC, unit)
         if (not force and os.path.exists(obj)
-                and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_header)):
+                and os.path.getmtime(obj) >= newest_dep(src)):
             return unit, obj, None
         cmd = [NVCC, *COMMON, *flags, "-c", os.path.join(SRC, unit), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
