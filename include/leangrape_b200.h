@@ -193,6 +193,12 @@ int lg_bench_zgemm(int32_t d, int32_t C, int32_t iters, double* ms_per_launch);
 
 /* "<engine>:<dominant backward kernel>" chosen for this problem (diagnostics, bench.py roofline). */
 const char* lg_engine_name(lg_problem* p);
+
+/* DIAGONALIZATION backend (src/derivatives.py:228-246, the np.linalg.eigh call): which per-step
+ * factorisation the last evaluation used -- "jacobi ..." (in shared memory, d <= 64),
+ * "jacobi-global ..." (hand-written, any d), "syevBatched" / "syevd" (LG_DIAG_LIB=1 A/B path);
+ * "" before the first evaluation or on the Taylor backend. */
+const char* lg_diag_solver_name(lg_problem* p);
 /* Device state vectors held per trajectory by this problem's engine (GradientResult.live_vector_peak,
  * src/costs.py:171-199); the same value lg_eval reports, also for sharded problems. */
 int64_t lg_live_vector_peak(lg_problem* p);

@@ -127,6 +127,8 @@ def load() -> C.CDLL:
     lib.lg_device_count.argtypes = []
     lib.lg_engine_name.argtypes = [P]
     lib.lg_engine_name.restype = C.c_char_p
+    lib.lg_diag_solver_name.argtypes = [P]
+    lib.lg_diag_solver_name.restype = C.c_char_p
     lib.lg_live_vector_peak.argtypes = [P]
     lib.lg_live_vector_peak.restype = C.c_int64
     lib.lg_launch_count.argtypes = []

@@ -332,6 +332,11 @@ class NativeProblem:
         """Sweep engine the library chose for this problem (lg_engine_name)."""
         return self._lib.lg_engine_name(self.handle).decode()
 
+    @property
+    def diag_solver(self) -> str:
+        """Per-step factorisation the last DIAGONALIZATION evaluation used (lg_diag_solver_name)."""
+        return self._lib.lg_diag_solver_name(self.handle).decode()
+
     def grad(self, a: ControlField) -> GradientResult:
         amps = np.ascontiguousarray(a.amplitudes, np.float64)
         cost = C.c_double()

@@ -467,6 +467,8 @@ const char* lg_engine_name(lg_problem* p) {
   }
 }
 
+const char* lg_diag_solver_name(lg_problem* p) { return p ? p->diag_solver : ""; }
+
 int lg_set_timing(lg_problem* p, int enable) {
   if (!p) return fail(LG_INVALID_ARG, "null problem handle");
   if (enable && !p->ev[0])

@@ -474,12 +474,14 @@ def golden_stress():
     save("stress", **out)
 
 
-def golden_diag(big=False):
+def golden_diag(big=False, mid=False):
     """The reference's DIAGONALIZATION backend (src/derivatives.py:228-275): every cost kind on a
     dense d = 40 problem (c1's model), a CSR d = 24 and a CSR d = 60 problem, random states,
     large amplitudes.  Sparse inputs stay CSR here: the reference densifies each step.
     big=True (``diag_big``): a CSR d = 180 problem (transmon 6 x cavity 30) and a dense d = 256
-    one, above the device CTA engine's d <= 128 (the dense GEMM engine applies the propagators)."""
+    one, above the device CTA engine's d <= 128 (the dense GEMM engine applies the propagators).
+    mid=True (``diag_mid``): a CSR d = 96 problem (transmon 4 x cavity 24): above the in-shared-memory
+    factorisation's d <= 64, still on the CTA engine."""
     out = {}
     rng = np.random.default_rng(7171)
     DIAG = derivatives.Backend.DIAGONALIZATION
@@ -513,6 +515,11 @@ def golden_diag(big=False):
             cost_state=cs, grad_state=gs, cost_state_only=css, cost_g1=cg1, grad_g1=gg1, cost_g3=cg3,
             grad_g3=gg3).items()})
 
+    if mid:
+        h_s, hx, hy = tc_ops(4, 24)
+        one("d_csr96", h_s, [hx, hy], 12, 0.5, 0.8, 2, 406)
+        save("diag_mid", **out)
+        return
     if big:
         h_s, hx, hy = tc_ops(6, 30)
         one("d_csr180", h_s, [hx, hy], 10, 0.5, 0.5, 2, 404)
@@ -531,6 +538,10 @@ def golden_diag(big=False):
 
 def golden_diag_big():
     golden_diag(big=True)
+
+
+def golden_diag_mid():
+    golden_diag(mid=True)
 
 
 BENCH_MU_CASES = [("transmon_cavity", 10, 0.1), ("transmon_cavity", 40, 0.5), ("transmon_cavity", 80, 2.0),

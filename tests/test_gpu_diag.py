@@ -23,16 +23,24 @@ def _check(res, cost, grad):
     assert G.grad_rel(res.grad, grad) <= GRAD_TOL, G.grad_rel(res.grad, grad)
 
 
-@pytest.mark.parametrize("golden,tag,engine", [("diag", "d_dense40", "cta"), ("diag", "d_csr24", "cta"),
-                                                ("diag", "d_csr60", "cta"), ("diag", "d_dense40", "dense-diag"),
-                                                ("diag", "d_csr60", "dense-diag"),
-                                                ("diag_big", "d_csr180", "dense-diag"),
-                                                ("diag_big", "d_dense256", "dense-diag")])
-def test_diagonalization_backend_matches_reference(golden, tag, engine, monkeypatch):
+@pytest.mark.parametrize("golden,tag,engine,solver", [
+    ("diag", "d_dense40", "cta", "jacobi"), ("diag", "d_csr24", "cta", "jacobi"), ("diag", "d_csr60", "cta", "jacobi"),
+    ("diag", "d_dense40", "dense-diag", "jacobi"), ("diag", "d_csr60", "dense-diag", "jacobi"),
+    ("diag_mid", "d_csr96", "cta", "jacobi-global"), ("diag_mid", "d_csr96", "dense-diag", "jacobi-global"),
+    ("diag_big", "d_csr180", "dense-diag", "jacobi-global"), ("diag_big", "d_dense256", "dense-diag", "jacobi-global"),
+    ("diag", "d_csr60", "cta", "lib"), ("diag_mid", "d_csr96", "cta", "lib"),
+    ("diag_big", "d_dense256", "dense-diag", "lib")])
+def test_diagonalization_backend_matches_reference(golden, tag, engine, solver, monkeypatch):
     """d <= 128: the CTA engine (one dense operator application per propagator); above (and with
-    LG_ENGINE=dense below): the dense GEMM engine, one DMMA GEMM per propagator application."""
+    LG_ENGINE=dense below): the dense GEMM engine, one DMMA GEMM per propagator application.
+    The per-step factorisation is hand-written at every d (in shared memory up to d = 64, in global
+    memory above); ``lib`` runs the cuSOLVER / cuBLAS A/B path (LG_DIAG_LIB=1) on the same vectors."""
     if engine == "dense-diag":
         monkeypatch.setenv("LG_ENGINE", "dense")
+    if solver == "lib":
+        monkeypatch.setenv("LG_DIAG_LIB", "1")
+    else:
+        monkeypatch.delenv("LG_DIAG_LIB", raising=False)
     z = G.sub(G.load(golden), tag)
     hs, hc = G.mats(z)
     om = G.penalty(z)
@@ -46,6 +54,8 @@ def test_diagonalization_backend_matches_reference(golden, tag, engine, monkeypa
     npb = NativeProblem(prob, terms, initial_states=z["psi0"])
     _check(npb.grad(a), z["cost_state"], z["grad_state"])
     assert npb.engine.startswith(engine), npb.engine
+    got = npb.diag_solver
+    assert got.startswith("syev") if solver == "lib" else got.split()[0] == solver, got
     assert abs(npb.cost(a) - float(z["cost_state_only"])) <= COST_TOL
     for kind, ck, gk in [(CostKind.GATE_INFIDELITY, "cost_g1", "grad_g1"),
                          (CostKind.GATE_RUNNING_INFIDELITY, "cost_g3", "grad_g3")]:
