@@ -48,6 +48,59 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 }  // namespace
 
+// 3M combine + split-k partial store or the fused Taylor epilogue for one warp's 16 x (8 NTT) tile
+template <int NTT>
+__device__ __forceinline__ void zgemm_finish(const LgGemmArgs& G, const double (&t1)[2][NTT][2],
+                                             const double (&t2)[2][NTT][2], const double (&t3)[2][NTT][2], int m0,
+                                             int n0, int warp, int r8, int q4) {
+  const int M = G.M, C = G.C;
+  double yr[2][NTT][2], yi[2][NTT][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NTT; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        yr[a][b][v] = t1[a][b][v] - t2[a][b][v];
+        yi[a][b][v] = (t3[a][b][v] - t1[a][b][v]) - t2[a][b][v];
+      }
+  if (G.ksplit > 1) {  // raw partial product of this k-slice
+    double2* P = G.partial + (long)blockIdx.z * M * C;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int m = m0 + warp * 16 + mt * 8 + r8;
+          const int n = n0 + nt * 8 + 2 * q4 + v;
+          if (m < M && n < C) P[(long)n * M + m] = make_double2(yr[mt][nt][v], yi[mt][nt][v]);
+        }
+    return;
+  }
+  // fused Taylor epilogue
+  const double r = G.r;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int m = m0 + warp * 16 + mt * 8 + r8;
+        const int n = n0 + nt * 8 + 2 * q4 + v;
+        if (m >= M || n >= C) continue;
+        const double2 tt = make_double2(yr[mt][nt][v] * r, yi[mt][nt][v] * r);
+        double2 base;
+        if (G.first)
+          base = G.xin ? G.xin[(long)n * G.ldxin + m] : make_double2(0.0, 0.0);
+        else
+          base = G.cur[(long)n * G.ldc + m];
+        const double2 cu = make_double2(base.x + tt.x, base.y + tt.y);
+        G.cur[(long)n * G.ldc + m] = cu;
+        G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
+      }
+}
+
 // grid (ceil(C / BN), ceil(M / BM), ksplit); 128 threads = 4 warps, each a 16 x BN tile,
 // BN = 8 NTT columns (NTT = 2 or 4: the wider tile halves the A-fragment loads per DMMA).
 // Dynamic shared memory: lg_zgemm_smem_bytes(NTT).
@@ -148,51 +201,7 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
     }
     __syncthreads();  // every warp done with buffer buf before tile t + 2 is copied into it
   }
-  double yr[2][NTT][2], yi[2][NTT][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < NTT; ++b)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        yr[a][b][v] = t1[a][b][v] - t2[a][b][v];
-        yi[a][b][v] = (t3[a][b][v] - t1[a][b][v]) - t2[a][b][v];
-      }
-  if (G.ksplit > 1) {  // raw partial product of this k-slice
-    double2* P = G.partial + (long)blockIdx.z * M * C;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NTT; ++nt)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int m = m0 + warp * 16 + mt * 8 + r8;
-          const int n = n0 + nt * 8 + 2 * q4 + v;
-          if (m < M && n < C) P[(long)n * M + m] = make_double2(yr[mt][nt][v], yi[mt][nt][v]);
-        }
-    return;
-  }
-  // fused Taylor epilogue
-  const double r = G.r;
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NTT; ++nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int m = m0 + warp * 16 + mt * 8 + r8;
-        const int n = n0 + nt * 8 + 2 * q4 + v;
-        if (m >= M || n >= C) continue;
-        const double2 tt = make_double2(yr[mt][nt][v] * r, yi[mt][nt][v] * r);
-        double2 base;
-        if (G.first)
-          base = G.xin ? G.xin[(long)n * G.ldxin + m] : make_double2(0.0, 0.0);
-        else
-          base = G.cur[(long)n * G.ldc + m];
-        const double2 cu = make_double2(base.x + tt.x, base.y + tt.y);
-        G.cur[(long)n * G.ldc + m] = cu;
-        G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
-      }
+  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4);
 }
 
 extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
@@ -202,6 +211,146 @@ extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor_n32(const __
   zgemm_taylor<4>(G);
 }
 extern "C" int lg_zgemm_smem_bytes(int ntt) { return (int)sizeof(double2) * 2 * (BK * SAM + 8 * ntt * SXK); }
+
+// ---------------------------------------------------------------------------------------------
+// Same tile and inner loop, Blackwell data movement: a PRODUCER warp moves the tiles with the TMA
+// engine's bulk copies (cp.async.bulk global -> shared, one per operand row: a k-row of the A tile is
+// BM contiguous complex, a column of the X tile BK contiguous complex, so plain 1-D bulk copies keep
+// the padded conflict-free strides and need no tensor map), completion by mbarrier complete_tx
+// bytes; the four CONSUMER warps wait on the stage's "full" barrier, run the 3M DMMA k-steps and
+// release the stage through its "empty" barrier: a STAGES-deep ring with no CTA barrier and no copy
+// instruction in the MMA warps.  Requires M % 64 == 0, C % (8 NTT) == 0, K % 16 == 0 per segment
+// (the host falls back to the cp.async kernel otherwise).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NTT, int STAGES>
+__device__ __forceinline__ void zgemm_taylor_bulk(const LgGemmArgs& G) {
+  constexpr int BN = 8 * NTT;
+  constexpr int A_ST = BK * SAM, X_ST = BN * SXK;  // complex elements per stage
+  double2* sA = zg_dsm;                    // [STAGES][BK][SAM]
+  double2* sX = zg_dsm + STAGES * A_ST;    // [STAGES][BN][SXK]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(zg_dsm + STAGES * (A_ST + X_ST));
+  unsigned long long* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int tiles0 = G.seg[0].K / BK;
+  const int all_tiles = tiles0 + (G.nseg > 1 ? G.seg[1].K / BK : 0);
+  const int t_lo = (int)((long)all_tiles * blockIdx.z / gridDim.z);
+  const int t_hi = (int)((long)all_tiles * (blockIdx.z + 1) / gridDim.z);
+  const int total = t_hi - t_lo;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 4) {  // producer
+    for (int tl = 0; tl < total; ++tl) {
+      const int st = tl % STAGES;
+      if (tl >= STAGES) mbar_wait(empty + st, (unsigned)((tl / STAGES - 1) & 1));
+      const int t = t_lo + tl;
+      const LgGemmSeg& S = G.seg[t < tiles0 ? 0 : 1];
+      const int k0 = (t < tiles0 ? t : t - tiles0) * BK;
+      if (lane == 0) mbar_expect_tx(full + st, (unsigned)((BK * BM + BN * BK) * sizeof(double2)));
+      __syncwarp();
+      double2* dA = sA + st * A_ST;
+      double2* dX = sX + st * X_ST;
+      for (int i = lane; i < BK + BN; i += 32) {
+        if (i < BK)
+          bulk_g2s(dA + i * SAM, S.A + (long)(k0 + i) * S.lda + m0, BM * sizeof(double2), full + st);
+        else
+          bulk_g2s(dX + (i - BK) * SXK, S.X + (long)(n0 + i - BK) * S.ldx + k0, BK * sizeof(double2), full + st);
+      }
+    }
+    return;
+  }
+  const int q4 = lane & 3, r8 = lane >> 2;
+  double t1[2][NTT][2], t2[2][NTT][2], t3[2][NTT][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NTT; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) t1[a][b][v] = t2[a][b][v] = t3[a][b][v] = 0.0;
+  for (int tl = 0; tl < total; ++tl) {
+    const int st = tl % STAGES;
+    mbar_wait(full + st, (unsigned)((tl / STAGES) & 1));
+    const double2* cA = sA + st * A_ST + q4 * SAM + warp * 16 + r8;
+    const double2* cX = sX + st * X_ST + r8 * SXK + q4;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[2], ai[2], sa[2], xr[NTT], xi[NTT], sx[NTT];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double2 a = cA[kk * SAM + mt * 8];
+        ar[mt] = a.x;
+        ai[mt] = a.y;
+        sa[mt] = a.x + a.y;
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt) {
+        const double2 x = cX[nt * 8 * SXK + kk];
+        xr[nt] = x.x;
+        xi[nt] = x.y;
+        sx[nt] = x.x + x.y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTT; ++nt) dmma(t1[mt][nt][0], t1[mt][nt][1], ar[mt], xr[nt]);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTT; ++nt) dmma(t2[mt][nt][0], t2[mt][nt][1], ai[mt], xi[nt]);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTT; ++nt) dmma(t3[mt][nt][0], t3[mt][nt][1], sa[mt], sx[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);  // this warp is done reading the stage
+  }
+  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4);
+}
+
+constexpr int LG_ZG_STAGES = 4;
+extern "C" __global__ void __launch_bounds__(160) lg_k_zgemm_taylor_bulk(const __grid_constant__ LgGemmArgs G) {
+  zgemm_taylor_bulk<4, LG_ZG_STAGES>(G);
+}
+extern "C" int lg_zgemm_bulk_smem_bytes() {
+  return (int)(sizeof(double2) * LG_ZG_STAGES * (BK * SAM + 32 * SXK) + 2 * LG_ZG_STAGES * sizeof(unsigned long long));
+}
+extern "C" void* lg_zgemm_bulk_kernel() { return (void*)lg_k_zgemm_taylor_bulk; }
 
 // Split-k finish: y = sum of the k-slices in slice order (deterministic), then the Taylor update.
 extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G) {

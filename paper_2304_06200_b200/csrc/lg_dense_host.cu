@@ -34,11 +34,41 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
   const int n32_from = ev ? std::atoi(ev) : 64;
   const int ntt = n32_from > 0 && C >= n32_from ? 4 : 2;
   const int bn = 8 * ntt;
-  const int smem = lg_zgemm_smem_bytes(ntt);
+  int smem = lg_zgemm_smem_bytes(ntt);
   void* kern = ntt == 4 ? lg_zgemm_n32_kernel() : lg_zgemm_kernel();
+  // aligned shapes (c5): the warp-specialised kernel whose tiles move by TMA bulk copies through a
+  // 4-stage mbarrier ring (producer warp + 4 MMA warps); LG_ZGEMM_BULK=0 keeps the cp.async kernel
+  static const bool bulk_on = !(std::getenv("LG_ZGEMM_BULK") && std::atoi(std::getenv("LG_ZGEMM_BULK")) == 0);
+  const bool bulk = bulk_on && ntt == 4 && d % 64 == 0 && C % 32 == 0;  // every segment has K = lda = d
+  int threads = 128;
+  if (bulk) {
+    kern = lg_zgemm_bulk_kernel();
+    smem = lg_zgemm_bulk_smem_bytes();
+    threads = 160;
+  }
   // (launch() raises the kernel's dynamic shared-memory limit to `smem` when it exceeds 48 KB)
   const long nct = (long)((C + bn - 1) / bn) * ((d + 63) / 64);
   int ks = (int)std::max<long>(1, std::min<long>(ntt == 4 ? 8 : 4, 2048L / std::max<long>(nct, 1)));
+  if (bulk) {
+    // the k-slices that fill whole waves of co-resident CTAs: minimise waves x (k-tiles per slice + ~2
+    // tiles of pipeline fill and epilogue); d = 4096: C = 64 -> 9 slices (37.1 vs 35.1 TF/s with 8),
+    // C = 128 -> 8 (LG_SPLITK sweep, tools/bench_zgemm.py)
+    static int slots = 0;
+    if (!slots) {
+      int dev = 0, sms = 148, occ = 2;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      ensure_smem(kern, smem);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 2;
+      slots = sms * occ;
+    }
+    const long tiles = (long)(d / 16) * (B ? 2 : 1);
+    long best = -1;
+    for (int k = 1; k <= 16; ++k) {
+      const long cost = ((nct * k + slots - 1) / slots) * ((tiles + k - 1) / k + 2);
+      if (best < 0 || cost < best) best = cost, ks = k;
+    }
+  }
   if (const char* e = std::getenv("LG_SPLITK")) ks = std::max(1, std::atoi(e));
   G.ksplit = ks;
   if (ks > 1) {
@@ -53,7 +83,7 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
     G.partial = p->d_splitws;
   }
   void* args[] = {&G};
-  int rc = launch(kern, dim3((C + bn - 1) / bn, (d + 63) / 64, ks), dim3(128), args, smem, p->stream);
+  int rc = launch(kern, dim3((C + bn - 1) / bn, (d + 63) / 64, ks), dim3(threads), args, smem, p->stream);
   if (rc || ks == 1) return rc;
   const long mc = (long)d * C;
   return launch(lg_taylor_epi_kernel(), dim3((unsigned)std::min<long>((mc + 255) / 256, 148 * 8)), dim3(256), args, 0,

@@ -2,6 +2,7 @@
 //   mode 0: 24 independent DMMAs per k-step (the 16 x 32 warp tile's 3M products), operands in registers
 //   mode 1: + the 6 DADDs forming the 3M operand sums
 //   mode 2: + 6 LDS.128 fragment loads from shared memory (the full inner loop without cp.async)
+//   mode 3: mode 2 with the next k-step's fragments loaded before this k-step's DMMAs (explicit prefetch)
 // Prints TFLOP/s (8x8x4x2 flops per DMMA) for CTAs of 128 threads at 1..4 CTAs per SM.
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -26,10 +27,28 @@ __global__ void __launch_bounds__(128) k(double* out, int iters, double seed) {
   double ar[2] = {seed, seed + 1}, ai[2] = {seed + 2, seed + 3};
   double xr[4] = {seed, seed * 2, seed * 3, seed * 4}, xi[4] = {seed, seed * 5, seed * 6, seed * 7};
   const int lane = threadIdx.x & 31;
-  int off = lane * 2;
+  int off = lane;  // 16-byte lane stride: conflict-free LDS.128, like the kernel's tile strides
+  double2 na[2], nx[4];
+  if (MODE == 3) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) na[m] = s[(off + m * 8) & 2047];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) nx[n] = s[(off + 512 + n * 80) & 2047];
+    off += 66;
+  }
   for (int it = 0; it < iters; ++it) {
     double sa[2], sx[4];
-    if (MODE >= 2) {
+    if (MODE == 3) {  // consume the prefetched fragments, then issue the next iteration's loads
+#pragma unroll
+      for (int m = 0; m < 2; ++m) { ar[m] = na[m].x; ai[m] = na[m].y; }
+#pragma unroll
+      for (int n = 0; n < 4; ++n) { xr[n] = nx[n].x; xi[n] = nx[n].y; }
+#pragma unroll
+      for (int m = 0; m < 2; ++m) na[m] = s[(off + m * 8) & 2047];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) nx[n] = s[(off + 512 + n * 80) & 2047];
+      off += 66;
+    } else if (MODE >= 2) {
 #pragma unroll
       for (int m = 0; m < 2; ++m) { const double2 v = s[(off + m * 8) & 2047]; ar[m] = v.x; ai[m] = v.y; }
 #pragma unroll
@@ -98,6 +117,7 @@ int main() {
   run<0>(out, sms);
   run<1>(out, sms);
   run<2>(out, sms);
+  run<3>(out, sms);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
