@@ -66,9 +66,10 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
   p->trp_reduced = false;
   if (p->engine == 3) {
     p->mark(1);
-    int rc = run_dense(p, N, p->cached_dt, grad);
+    p->dense_bwd_marked = false;
+    int rc = run_dense(p, N, p->cached_dt, grad);  // records the forward / backward boundary itself
     if (rc) return rc;
-    p->mark(2);
+    if (!p->dense_bwd_marked) p->mark(2);
     rc = hook_raw(p, N);
     if (rc) return rc;
     p->mark(3);

@@ -409,7 +409,9 @@ int run_dense(lg_problem* p, long N, double dt, bool grad) {
       }
       if (rc) return rc;
     }
-    // ---- backward sweep
+    // ---- backward sweep (phase event: with several trajectory sets the last set's boundary is kept)
+    p->mark(2);
+    p->dense_bwd_marked = true;
     int gch[LG_MAX_CHANNELS];
     for (long n = N - 1; n >= 0; --n) {
       const int4* pn = &pl[(size_t)n * (Kc + 1)];

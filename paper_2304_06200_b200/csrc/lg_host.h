@@ -145,6 +145,7 @@ struct lg_problem {
   int engine = 0;  // 0 legacy single-CTA, 1 legacy multi-CTA (grid barrier), 2 cta engine, 3 dense GEMM
   bool dense_large = false;
   bool diag_dense = false;  // DIAGONALIZATION backend on the dense GEMM engine (d > 128)
+  bool dense_bwd_marked = false;  // run_dense recorded the forward / backward phase event of this evaluation
   // dense GEMM engine buffers
   double2* d_Ad = nullptr;           // dense engine: A_n = -i dt H_n, interleaved, column-major
   std::vector<double2*> d_Acd;       // A_c = -i dt h_c per channel
