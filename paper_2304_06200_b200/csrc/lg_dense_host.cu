@@ -38,7 +38,8 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
   void* kern = ntt == 4 ? lg_zgemm_n32_kernel() : lg_zgemm_kernel();
   // aligned shapes (c5): the warp-specialised kernel whose tiles move by TMA bulk copies through a
   // 4-stage mbarrier ring (producer warp + 4 MMA warps); LG_ZGEMM_BULK=0 keeps the cp.async kernel
-  static const bool bulk_on = !(std::getenv("LG_ZGEMM_BULK") && std::atoi(std::getenv("LG_ZGEMM_BULK")) == 0);
+  const char* eb = std::getenv("LG_ZGEMM_BULK");
+  const bool bulk_on = !(eb && std::atoi(eb) == 0);
   const bool bulk = bulk_on && ntt == 4 && d % 64 == 0 && C % 32 == 0;  // every segment has K = lda = d
   int threads = 128;
   if (bulk) {

@@ -3,10 +3,14 @@
 * c3 at full size (N=2000, K=8): golden ``c3_full.npz`` = the reference's composite_grad per state
   (src/costs.py:515-546 -> _state_pass :269-354), summed in state order (make_golden.py).
 * c5 with ALL K=64 states on an N'=2 prefix: the full-K dense engine path.  Its forward chain has
-  64 columns and its adjoint / aux chains 128 / 64, so every Taylor GEMM runs the wide-tile kernel
-  ``lg_k_zgemm_taylor_n32`` with split-k 8 (lg_dense_host.cu: chosen from 64 columns) -- the
-  kernel every full-size c5 evaluation executes (DenseMatrix.matvec, src/sparse.py:193-199, inside
-  expm.apply, src/expm.py:345-350).
+  64 columns and its adjoint / aux chains 128 / 64, so every Taylor GEMM runs the wide-tile kernels
+  every full-size c5 evaluation executes (DenseMatrix.matvec, src/sparse.py:193-199, inside
+  expm.apply, src/expm.py:345-350): by default the TMA bulk-copy kernel ``lg_k_zgemm_taylor_bulk``
+  (tile-aligned shapes) with its wave-filling split-k, and -- parametrised -- the same kernel without
+  split-k (fused Taylor epilogue) and with an uneven split, and the cp.async kernel
+  ``lg_k_zgemm_taylor_n32`` (LG_ZGEMM_BULK=0) with split-k 8.
+* c4 at full size: engine agreement (below) and the directional derivative of the cost against the
+  gradient, a size-independent property (the reference needs ~21 h for this configuration).
 * The same dense cases with the wide tile forced from 1 column (LG_ZGEMM_N32=1) and with split-k
   forced off / to 8, so both GEMM kernels and the split-k epilogue meet every dense golden.
 
@@ -37,7 +41,12 @@ def test_c3_full_size_against_reference():
     _check(composite_grad(case.problem, case.field, case.terms), z["cost"], z["grad"])
 
 
-def test_c5_all_64_states_full_k_gemm_path():
+@pytest.mark.parametrize("bulk,splitk", [(None, None), ("1", "1"), ("1", "5"), ("0", None)])
+def test_c5_all_64_states_full_k_gemm_path(bulk, splitk, monkeypatch):
+    if bulk is not None:
+        monkeypatch.setenv("LG_ZGEMM_BULK", bulk)
+    if splitk is not None:
+        monkeypatch.setenv("LG_SPLITK", splitk)
     z = G.load("c5_fullk")
     n = int(z["n_prefix"])
     case = models.build_case("c5", n_steps=n, n_states=64)
@@ -107,3 +116,27 @@ def test_c4_full_size_engine_agreement(monkeypatch):
     assert eng_g.startswith("cluster") and "large" not in eng_g, eng_g
     assert abs(res_g.cost - res.cost) <= COST_TOL
     assert G.grad_rel(res_g.grad, res.grad) <= 1e-10
+
+
+def test_c4_full_size_directional_derivative():
+    """Size-independent property at the bench configuration's full size: along a random direction v
+    of the control field, the central difference of composite_cost (forward sweeps only) matches
+    grad . v from composite_grad (forward + two-phase backward).  The two sides share only the
+    forward sweep, so this pins the adjoint sweep and the derivative-product items of all 32
+    trajectories and 4000 steps against the cost itself."""
+    from paper_2304_06200_b200 import composite_cost
+
+    case = models.build_case("c4")
+    res = composite_grad(case.problem, case.field, case.terms)
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal(res.grad.shape)
+    v /= np.linalg.norm(v)
+    # a direction with a gradient component, so the derivative is well above the FD noise floor
+    v = 0.5 * v + 0.5 * res.grad / max(np.linalg.norm(res.grad), 1e-300)
+    eps = 1e-4
+    a0 = case.field.amplitudes
+    cp = composite_cost(case.problem, case.field.replace_amplitudes(a0 + eps * v), case.terms)
+    cm = composite_cost(case.problem, case.field.replace_amplitudes(a0 - eps * v), case.terms)
+    fd = (cp - cm) / (2 * eps)
+    gv = float(np.sum(res.grad * v))
+    assert abs(fd - gv) <= 1e-5 * abs(gv) + 1e-11, (fd, gv)
