@@ -48,11 +48,79 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 }  // namespace
 
-// 3M combine + split-k partial store or the fused Taylor epilogue for one warp's 16 x (8 NTT) tile
+// Block coordinates: output tile (bx, by) and k-slice bz of nz.  With G.zfast the slices of one tile
+// are the fastest grid dimension, so they run together and the tile's last-arriving slice (fused
+// split-k finish below) reduces it while other tiles are still in their k loops.
+struct ZgIdx {
+  int bx, by, bz, nz;
+};
+__device__ __forceinline__ ZgIdx zg_idx(const LgGemmArgs& G) {
+  if (G.zfast) return ZgIdx{(int)blockIdx.y, (int)blockIdx.z, (int)blockIdx.x, (int)gridDim.x};
+  return ZgIdx{(int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)gridDim.z};
+}
+__device__ __forceinline__ void zg_bar_mma() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// Fused split-k finish (the tile's last-arriving slice): sum the slices IN SLICE ORDER from L2
+// (ld.global.cg) and apply the Taylor update -- the same order and arithmetic as lg_k_taylor_epi, so
+// both paths are bit-identical and deterministic.  Not inlined: the k loop keeps its register budget.
+template <int NTT>
+__device__ __noinline__ void zgemm_reduce_tile(const LgGemmArgs& G, int m0, int n0, int warp, int r8, int q4) {
+  const int M = G.M, C = G.C;
+  const long MC = (long)M * C;
+  const double r = G.r;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int m = m0 + warp * 16 + mt * 8 + r8;
+    double2 y[NTT][2];
+    long off[NTT][2];
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int n = n0 + nt * 8 + 2 * q4 + v;
+        off[nt][v] = m < M && n < C ? (long)n * M + m : -1;
+        y[nt][v] = off[nt][v] >= 0 ? __ldcg(G.partial + off[nt][v]) : make_double2(0.0, 0.0);
+      }
+    for (int z = 1; z < G.ksplit; ++z) {
+      const double2* Pz = G.partial + (long)z * MC;
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          if (off[nt][v] >= 0) {
+            const double2 pz = __ldcg(Pz + off[nt][v]);
+            y[nt][v].x += pz.x;
+            y[nt][v].y += pz.y;
+          }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        if (off[nt][v] < 0) continue;
+        const int n = n0 + nt * 8 + 2 * q4 + v;
+        const double2 tt = make_double2(y[nt][v].x * r, y[nt][v].y * r);
+        double2 base;
+        if (G.first)
+          base = G.xin ? G.xin[(long)n * G.ldxin + m] : make_double2(0.0, 0.0);
+        else
+          base = G.cur[(long)n * G.ldc + m];
+        const double2 cu = make_double2(base.x + tt.x, base.y + tt.y);
+        G.cur[(long)n * G.ldc + m] = cu;
+        G.tout[(long)n * G.ldt + m] = G.last ? cu : tt;
+      }
+  }
+}
+
+// 3M combine + split-k partial store or the fused Taylor epilogue for one warp's 16 x (8 NTT) tile.
+// Split-k with G.tile_ctr: every slice stores its partial tile, fences and counts itself on the
+// tile's counter; the last one to arrive reduces the tile (zgemm_reduce_tile) and resets the counter
+// for the next launch.
 template <int NTT>
 __device__ __forceinline__ void zgemm_finish(const LgGemmArgs& G, const double (&t1)[2][NTT][2],
                                              const double (&t2)[2][NTT][2], const double (&t3)[2][NTT][2], int m0,
-                                             int n0, int warp, int r8, int q4) {
+                                             int n0, int warp, int r8, int q4, const ZgIdx& B) {
+  __shared__ int s_last;
   const int M = G.M, C = G.C;
   double yr[2][NTT][2], yi[2][NTT][2];
 #pragma unroll
@@ -65,7 +133,7 @@ __device__ __forceinline__ void zgemm_finish(const LgGemmArgs& G, const double (
         yi[a][b][v] = (t3[a][b][v] - t1[a][b][v]) - t2[a][b][v];
       }
   if (G.ksplit > 1) {  // raw partial product of this k-slice
-    double2* P = G.partial + (long)blockIdx.z * M * C;
+    double2* P = G.partial + (long)B.bz * M * C;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -76,6 +144,19 @@ __device__ __forceinline__ void zgemm_finish(const LgGemmArgs& G, const double (
           const int n = n0 + nt * 8 + 2 * q4 + v;
           if (m < M && n < C) P[(long)n * M + m] = make_double2(yr[mt][nt][v], yi[mt][nt][v]);
         }
+    if (!G.tile_ctr) return;  // lg_k_taylor_epi finishes
+    __threadfence();
+    zg_bar_mma();
+    if (threadIdx.x == 0) {
+      int* ctr = G.tile_ctr + B.by * ((C + 8 * NTT - 1) / (8 * NTT)) + B.bx;
+      const int prev = atomicAdd(ctr, 1);
+      s_last = prev == G.ksplit - 1;
+      if (s_last) *ctr = 0;
+    }
+    zg_bar_mma();
+    if (!s_last) return;
+    __threadfence();
+    zgemm_reduce_tile<NTT>(G, m0, n0, warp, r8, q4);
     return;
   }
   // fused Taylor epilogue
@@ -112,7 +193,8 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
   double2* sX = zg_dsm + 2 * A_ST;   // [2][BN][SXK]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q4 = lane & 3, r8 = lane >> 2;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const ZgIdx B = zg_idx(G);
+  const int n0 = B.bx * BN, m0 = B.by * BM;
   const int M = G.M, C = G.C;
   double t1[2][NTT][2], t2[2][NTT][2], t3[2][NTT][2];
 #pragma unroll
@@ -125,8 +207,8 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
   // flattened k-tiles over the segments; this CTA's slice [t_lo, t_hi)
   const int tiles0 = (G.seg[0].K + BK - 1) / BK;
   const int all_tiles = tiles0 + (G.nseg > 1 ? (G.seg[1].K + BK - 1) / BK : 0);
-  const int t_lo = (int)((long)all_tiles * blockIdx.z / gridDim.z);
-  const int t_hi = (int)((long)all_tiles * (blockIdx.z + 1) / gridDim.z);
+  const int t_lo = (int)((long)all_tiles * B.bz / B.nz);
+  const int t_hi = (int)((long)all_tiles * (B.bz + 1) / B.nz);
   const int total = t_hi - t_lo;
 
   auto load_tile = [&](int tl, int buf) {
@@ -201,7 +283,7 @@ __device__ __forceinline__ void zgemm_taylor(const LgGemmArgs& G) {
     }
     __syncthreads();  // every warp done with buffer buf before tile t + 2 is copied into it
   }
-  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4);
+  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4, B);
 }
 
 extern "C" __global__ void __launch_bounds__(128) lg_k_zgemm_taylor(const __grid_constant__ LgGemmArgs G) {
@@ -260,11 +342,12 @@ __device__ __forceinline__ void zgemm_taylor_bulk(const LgGemmArgs& G) {
   unsigned long long* full = reinterpret_cast<unsigned long long*>(zg_dsm + STAGES * (A_ST + X_ST));
   unsigned long long* empty = full + STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const ZgIdx B = zg_idx(G);
+  const int n0 = B.bx * BN, m0 = B.by * BM;
   const int tiles0 = G.seg[0].K / BK;
   const int all_tiles = tiles0 + (G.nseg > 1 ? G.seg[1].K / BK : 0);
-  const int t_lo = (int)((long)all_tiles * blockIdx.z / gridDim.z);
-  const int t_hi = (int)((long)all_tiles * (blockIdx.z + 1) / gridDim.z);
+  const int t_lo = (int)((long)all_tiles * B.bz / B.nz);
+  const int t_hi = (int)((long)all_tiles * (B.bz + 1) / B.nz);
   const int total = t_hi - t_lo;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -340,7 +423,7 @@ __device__ __forceinline__ void zgemm_taylor_bulk(const LgGemmArgs& G) {
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);  // this warp is done reading the stage
   }
-  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4);
+  zgemm_finish<NTT>(G, t1, t2, t3, m0, n0, warp, r8, q4, B);
 }
 
 constexpr int LG_ZG_STAGES = 4;

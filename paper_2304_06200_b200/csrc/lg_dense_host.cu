@@ -83,9 +83,28 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
     }
     G.partial = p->d_splitws;
   }
+  // LG_ZGEMM_FUSEDK=1 (A/B knob, off by default): fused split-k finish -- every slice counts itself on
+  // its tile's counter and the last one to arrive reduces the tile and applies the Taylor update, so
+  // lg_k_taylor_epi's launch disappears; LG_ZGEMM_ZFAST=0 keeps the slice index on blockIdx.z instead
+  // of co-scheduling a tile's slices.  Measured at d = 4096 (tools/bench_zgemm.py, same box): 0.267 /
+  // 0.482 ms (slices co-scheduled) and 0.252 / 0.455 ms (slice index slowest) against 0.2275 / 0.4375 ms
+  // for the two-kernel path at 64 / 128 columns: the per-slice fence + counter round trip and the
+  // reduction on the tail of the last CTAs cost more than the 16 us epilogue kernel they replace.
+  constexpr int kCtrCap = 4096;
+  const char* ef = std::getenv("LG_ZGEMM_FUSEDK");
+  const bool fused = ks > 1 && nct <= kCtrCap && ef && std::atoi(ef) == 1;
+  if (fused && !p->d_tilectr) {
+    if (cudaMalloc(&p->d_tilectr, kCtrCap * sizeof(int)) != cudaSuccess) return fail(LG_CUDA_ERROR, "split-k tile counters");
+    if (cudaMemsetAsync(p->d_tilectr, 0, kCtrCap * sizeof(int), p->stream) != cudaSuccess)
+      return fail(LG_CUDA_ERROR, "split-k tile counters");
+  }
+  G.tile_ctr = fused ? p->d_tilectr : nullptr;
+  const char* ez = std::getenv("LG_ZGEMM_ZFAST");
+  G.zfast = fused && !(ez && std::atoi(ez) == 0) ? 1 : 0;
   void* args[] = {&G};
-  int rc = launch(kern, dim3((C + bn - 1) / bn, (d + 63) / 64, ks), dim3(threads), args, smem, p->stream);
-  if (rc || ks == 1) return rc;
+  const dim3 grid = G.zfast ? dim3(ks, (C + bn - 1) / bn, (d + 63) / 64) : dim3((C + bn - 1) / bn, (d + 63) / 64, ks);
+  int rc = launch(kern, grid, dim3(threads), args, smem, p->stream);
+  if (rc || ks == 1 || fused) return rc;
   const long mc = (long)d * C;
   return launch(lg_taylor_epi_kernel(), dim3((unsigned)std::min<long>((mc + 255) / 256, 148 * 8)), dim3(256), args, 0,
                 p->stream);

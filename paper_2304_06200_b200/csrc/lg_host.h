@@ -160,6 +160,7 @@ struct lg_problem {
   int ws_nw = 1;  // derivative workers per channel in the cluster backward
   double2* d_splitws = nullptr;  // dense engine split-k workspace (cudaMalloc'd, freed in ~lg_problem)
   size_t splitws_cap = 0;
+  int* d_tilectr = nullptr;  // dense engine: per-tile arrival counters of the fused split-k finish
   // cluster engine
   int cl_split = 0, cl_R_b = 0, cl_Q_b = 1, cl_E_b = 0, cl_T_b = 0, cl_smem_split = 0;  // split backward
   int cl_CS = 0, cl_R = 0, cl_H = 0, cl_Q = 1, cl_E = 0, cl_small = 0, cl_maxc = 0, cl_smem = 0, cl_smem_b = 0, cl_acs = 0;
@@ -258,6 +259,7 @@ struct lg_problem {
     bkmem.release();
     mem.release();
     if (d_splitws) cudaFree(d_splitws);
+    if (d_tilectr) cudaFree(d_tilectr);
     if (stream2) cudaStreamDestroy(stream2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);

@@ -173,6 +173,8 @@ struct LgGemmArgs {
   int first, last;
   int ksplit;  // lg_dense.cu: split-k slices (partial products in `partial`)
   double2* partial;
+  int* tile_ctr;  // per-output-tile arrival counters (zeroed; the last slice resets): fused split-k finish
+  int zfast;      // k-slice index on blockIdx.x (slices of a tile co-scheduled) instead of blockIdx.z
 };
 struct LgDotArgs {
   int d, n;

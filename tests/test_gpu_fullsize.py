@@ -59,6 +59,27 @@ def test_c5_all_64_states_full_k_gemm_path(bulk, splitk, monkeypatch):
     assert abs(npb.cost(case.field) - float(z["cost"])) <= COST_TOL
 
 
+@pytest.mark.parametrize("bulk", ["1", "0"])
+@pytest.mark.parametrize("zfast", ["1", "0"])
+def test_c5_fused_split_k_finish_is_bit_identical(bulk, zfast, monkeypatch):
+    """LG_ZGEMM_FUSEDK=1 (the tile's last-arriving k-slice reduces it in slice order inside the GEMM)
+    against the default two-kernel split-k path: same sums in the same order, so identical bits."""
+    z = G.load("c5_fullk")
+    case = models.build_case("c5", n_steps=int(z["n_prefix"]), n_states=64)
+    monkeypatch.setenv("LG_ZGEMM_BULK", bulk)
+
+    def run():
+        return NativeProblem(case.problem, case.terms, initial_states=case.problem.initial_state).grad(case.field)
+
+    base = run()
+    monkeypatch.setenv("LG_ZGEMM_FUSEDK", "1")
+    monkeypatch.setenv("LG_ZGEMM_ZFAST", zfast)
+    fused = run()
+    assert fused.cost == base.cost
+    assert np.array_equal(fused.grad, base.grad)
+    _check(fused, z["cost"], z["grad"])
+
+
 @pytest.mark.parametrize("n32,splitk", [("1", None), ("1", "1"), ("0", "8"), ("1", "8")])
 def test_dense_goldens_with_forced_gemm_tiles(n32, splitk, monkeypatch):
     monkeypatch.setenv("LG_ZGEMM_N32", n32)
