@@ -28,7 +28,7 @@ from enum import Enum
 import numpy as np
 
 from . import _native
-from .sparse import DenseMatrix, as_own_matrix, frozen_copy, is_hermitian, one_norm_host, to_dense
+from .sparse import DenseMatrix, as_own_matrix, frozen_copy, is_hermitian, linear_combine, one_norm_host, to_dense
 
 __all__ = [
     "Backend",
@@ -131,6 +131,15 @@ class ControlProblem:
                 raise ValueError(f"control operator {k} has mismatched shape")
             if not is_hermitian(hc, 1e-12 * max(1.0, one_norm_host(hc))):
                 raise ValueError(f"control operator {k} is not Hermitian")
+
+    def step_evaluator(self, a: "ControlField", n: int):
+        """The reference's per-step evaluator (src/costs.py:131-138): step n's amplitudes folded into
+        H_n, actions evaluated on the device (derivatives.StepEvaluator)."""
+        from .derivatives import StepContext, StepEvaluator
+
+        coeffs = [1.0] + [complex(x) for x in a.amplitudes[n]]
+        h_step = linear_combine(coeffs, [self.h_static, *self.h_controls])
+        return StepEvaluator(StepContext(h_step, self.h_controls, a.dt, self.backend, self.tau, validate=False))
 
     @property
     def dim(self) -> int:

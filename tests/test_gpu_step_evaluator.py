@@ -1,0 +1,177 @@
+"""The per-step surface (``ControlProblem.step_evaluator``, ``derivatives.propagate`` ...; reference
+src/derivatives.py:113-225,278-330, exercised there by pkg/tests/test_derivatives.py) evaluated on
+the device: closed forms, adjoint round trips, backend agreement, the derivative product against
+central differences and a commuting closed form, the block-operator plan path (2 d > 256) against the
+materialised embedding, and the hard-coded gradient re-assembled from the three per-step actions
+against ``c1_state_grad``.  Tolerances: tau = 1e-12 plans, 1e-10 on closed forms, 1e-6 relative on
+finite differences (step 1e-6), 1e-9 relative on the re-assembled gradient."""
+
+import numpy as np
+import pytest
+
+from paper_2304_06200_b200 import costs, derivatives, expm, sparse
+from paper_2304_06200_b200.costs import Backend, ControlField, ControlProblem
+from paper_2304_06200_b200.derivatives import StepContext, StepEvaluator
+
+pytestmark = pytest.mark.gpu
+
+SX = np.array([[0.0, 1.0], [1.0, 0.0]], np.complex128)
+SZ = np.array([[1.0, 0.0], [0.0, -1.0]], np.complex128)
+
+
+def _herm(g, d, scale=1.0):
+    z = g.standard_normal((d, d)) + 1j * g.standard_normal((d, d))
+    return scale * (z + z.conj().T) / 2
+
+
+def _ket(g, d):
+    v = g.standard_normal(d) + 1j * g.standard_normal(d)
+    return v / np.linalg.norm(v)
+
+
+def _exact(h, dt, psi):
+    w, v = np.linalg.eigh(h)
+    return v @ (np.exp(-1j * w * dt) * (v.conj().T @ psi))
+
+
+@pytest.fixture
+def g():
+    return np.random.default_rng(7731)
+
+
+def test_empty_step_hamiltonian_leaves_the_state(g):
+    d = 5
+    ctx = StepContext(sparse.build_csr([], d, d), (sparse.identity_csr(d),), 0.4, tau=1e-12)
+    psi = _ket(g, d)
+    assert np.allclose(derivatives.propagate(ctx, psi), psi, atol=1e-14)
+    assert np.allclose(derivatives.propagate_adjoint(ctx, psi), psi, atol=1e-14)
+
+
+def test_half_rabi_period_flips_with_the_right_phase():
+    omega = 0.8
+    ctx = StepContext(sparse.from_dense(0.5 * omega * SX), (sparse.from_dense(SX),), np.pi / omega, tau=1e-12)
+    out = derivatives.propagate(ctx, np.array([1.0, 0.0], complex))
+    assert abs(out[0]) <= 1e-10 and abs(out[1] + 1j) <= 1e-10
+
+
+@pytest.mark.parametrize("d", [6, 40])
+def test_both_backends_propagate_alike_and_match_the_eigen_solution(g, d):
+    h = _herm(g, d, 0.7)
+    psi = _ket(g, d)
+    outs = []
+    for backend in (Backend.SCALING_SQUARING, Backend.DIAGONALIZATION):
+        ctx = StepContext(sparse.from_dense(h), (sparse.from_dense(_herm(g, d)),), 0.3, backend, 1e-12)
+        outs.append((derivatives.propagate(ctx, psi), derivatives.propagate_adjoint(ctx, psi)))
+    want_f, want_a = _exact(h, 0.3, psi), _exact(h, -0.3, psi)
+    for f, a in outs:
+        assert np.abs(f - want_f).max() <= 1e-10
+        assert np.abs(a - want_a).max() <= 1e-10
+
+
+def test_non_hermitian_step_is_rejected(g):
+    bad = sparse.build_csr([(0, 1, 1.0)], 3, 3)
+    with pytest.raises(ValueError, match="Hermitian"):
+        StepContext(bad, (sparse.identity_csr(3),), 0.1)
+    with pytest.raises(ValueError, match="dt"):
+        StepContext(sparse.identity_csr(3), (sparse.identity_csr(3),), 0.0)
+
+
+def test_adjoint_undoes_forward(g):
+    d = 9
+    ev = StepEvaluator(StepContext(sparse.from_dense(_herm(g, d)), (sparse.from_dense(_herm(g, d)),), 0.25, tau=1e-12))
+    psi = _ket(g, d)
+    assert np.abs(ev.adjoint(ev.forward(psi)) - psi).max() <= 1e-10
+
+
+def test_empty_control_has_zero_derivative(g):
+    d = 4
+    ctx = StepContext(sparse.from_dense(_herm(g, d)), (sparse.build_csr([], d, d),), 0.3, tau=1e-12)
+    du, u = derivatives.derivative_action_aux(ctx, 0, _ket(g, d))
+    assert np.abs(du).max() == 0.0
+    assert abs(np.linalg.norm(u) - 1.0) <= 1e-10
+
+
+def test_commuting_control_closed_form(g):
+    # [H, h_c] = 0: dU/da = -i dt h_c U
+    dt, psi = 0.35, _ket(g, 2)
+    ctx = StepContext(sparse.from_dense(0.6 * SZ), (sparse.from_dense(SZ),), dt, tau=1e-12)
+    du, u = derivatives.derivative_action_aux(ctx, 0, psi)
+    assert np.abs(u - _exact(0.6 * SZ, dt, psi)).max() <= 1e-10
+    assert np.abs(du - (-1j * dt) * (SZ @ u)).max() <= 1e-10
+
+
+def test_derivative_product_matches_central_differences(g):
+    d, dt, a, eps = 7, 0.3, 0.4, 1e-6
+    hs, hc, psi = _herm(g, d), _herm(g, d), _ket(g, d)
+    problem = ControlProblem(sparse.from_dense(hs), (sparse.from_dense(hc),), tau=1e-12)
+    ev = problem.step_evaluator(ControlField.constant(a, 1, 1, dt), 0)
+    du = ev.control_derivative(0, psi)
+    fd = (_exact(hs + (a + eps) * hc, dt, psi) - _exact(hs + (a - eps) * hc, dt, psi)) / (2 * eps)
+    assert np.linalg.norm(du - fd) <= 1e-6 * np.linalg.norm(fd)
+
+
+def test_channel_index_is_checked(g):
+    ctx = StepContext(sparse.from_dense(_herm(g, 3)), (sparse.from_dense(_herm(g, 3)),), 0.2)
+    with pytest.raises(IndexError):
+        derivatives.derivative_action_aux(ctx, 1, _ket(g, 3))
+    with pytest.raises(IndexError):
+        StepEvaluator(ctx).control_derivative(-1, _ket(g, 3))
+    with pytest.raises(ValueError, match="dimension"):
+        derivatives.propagate(ctx, _ket(g, 4))
+
+
+def test_block_operator_bounds_and_action_match_the_materialised_embedding(g):
+    # 2 d = 280 > 256: the plan comes from the block operator's assembled bounds (one extra sigma' unit);
+    # the action must agree with the materialised embedding under its own plan
+    d, dt = 140, 0.2
+    band = np.zeros((d, d), complex)
+    for o in (1, 3):
+        v = 0.5 * (g.standard_normal(d - o) + 1j * g.standard_normal(d - o))
+        band[np.arange(d - o), np.arange(d - o) + o] = v
+        band[np.arange(d - o) + o, np.arange(d - o)] = v.conj()
+    band[np.arange(d), np.arange(d)] = g.standard_normal(d)
+    hc = np.diag(g.standard_normal(d)).astype(complex)
+    ctx = StepContext(sparse.from_dense(band), (sparse.from_dense(hc),), dt, tau=1e-12)
+    blk = derivatives.BlockDerivativeOperator(ctx.h_step.scaled(-1j * dt), ctx.h_controls[0], dt)
+    mat = derivatives.aux_embed(ctx.h_step, ctx.h_controls[0], dt)
+    assert blk.one_norm() == pytest.approx(mat.one_norm(), rel=1e-14)
+    assert blk.inf_norm() == pytest.approx(mat.inf_norm(), rel=1e-14)
+    assert blk.max_row_nnz() == mat.max_row_nnz() + 1
+    assert np.array_equal(blk.stored().to_dense(), mat.to_dense())
+    psi = _ket(g, d)
+    du, u = derivatives.derivative_action_aux(ctx, 0, psi)
+    stacked = np.zeros(2 * d, complex)
+    stacked[d:] = psi
+    ref = expm.apply(mat, stacked, derivatives.aux_plan(mat, 1e-12), validate=False)
+    assert np.abs(du - ref[:d]).max() <= 1e-11
+    assert np.abs(u - ref[d:]).max() <= 1e-11
+
+
+def test_diagonalization_derivative_is_refused_not_computed_on_the_host(g):
+    ctx = StepContext(sparse.from_dense(_herm(g, 4)), (sparse.from_dense(_herm(g, 4)),), 0.2, Backend.DIAGONALIZATION)
+    with pytest.raises(NotImplementedError):
+        StepEvaluator(ctx).control_derivative(0, _ket(g, 4))
+
+
+def test_stepwise_forward_equals_the_sweep_and_rebuilds_the_gradient(g):
+    d, n, k, dt = 8, 5, 2, 0.3
+    psi0, phi = _ket(g, d), _ket(g, d)
+    problem = ControlProblem(sparse.from_dense(_herm(g, d)), tuple(sparse.from_dense(_herm(g, d)) for _ in range(k)),
+                             tau=1e-12)
+    field = ControlField(n, k, dt, g.normal(scale=0.5, size=(n, k)))
+    evs = [problem.step_evaluator(field, i) for i in range(n)]
+    states = [psi0]
+    for ev in evs:
+        states.append(ev.forward(states[-1]))
+    assert np.abs(states[-1] - costs.forward_propagate(problem, field, psi0)).max() <= 1e-12
+    # hard-coded gradient of 1 - |<phi|psi_N>|^2 from the per-step actions (PAPER eq. for C1^st)
+    overlap = np.vdot(phi, states[-1])
+    lam = phi.copy()
+    grad = np.zeros((n, k))
+    for i in range(n - 1, -1, -1):
+        for c in range(k):
+            grad[i, c] = -2.0 * np.real(np.conj(overlap) * np.vdot(lam, evs[i].control_derivative(c, states[i])))
+        lam = evs[i].adjoint(lam)
+    res = costs.c1_state_grad(problem, field, psi0, phi)
+    assert res.cost == pytest.approx(1.0 - abs(overlap) ** 2, abs=1e-12)
+    assert np.linalg.norm(grad - res.grad) <= 1e-9 * np.linalg.norm(res.grad)
