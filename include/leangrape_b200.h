@@ -121,6 +121,14 @@ int lg_plan_table(lg_problem* p, int64_t n_steps, double dt, const double* amps,
  * (forward_propagate, src/costs.py:209-217). */
 int lg_forward_states(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* out);
 
+/* (dU_step / da_channel) psi of a DIAGONALIZATION problem, [2 d]: the per-step derivative product of
+ * the reference's eigenbasis formula (derivative_action_diag, src/derivatives.py:256-275, as
+ * StepEvaluator.control_derivative calls it, :317-320), from the device factorisation of the
+ * field's steps.  LG_UNSUPPORTED for Taylor problems (their product is lg_expm_apply on the embedded
+ * generator), LG_INDEX_ERROR for a step or channel out of range. */
+int lg_step_derivative(lg_problem* p, int64_t n_steps, double dt, const double* amps, int64_t step, int32_t channel,
+                       const double* psi, double* out);
+
 /* Raw per-trajectory scalars of the last evaluation (for sharded runs: the
  * partial sums every rank contributes; summing them across ranks and calling
  * lg_finalize_host reproduces the single-process result exactly). */

@@ -26,7 +26,7 @@ LG_UNSUPPORTED = 6
 
 EXPORTED = (
     "lg_problem_create", "lg_problem_destroy", "lg_eval", "lg_cost", "lg_cost_batch", "lg_eval_device", "lg_plan_table",
-    "lg_forward_states", "lg_raw_size", "lg_raw_get", "lg_finalize_host", "lg_make_plan",
+    "lg_forward_states", "lg_step_derivative", "lg_raw_size", "lg_raw_get", "lg_finalize_host", "lg_make_plan",
     "lg_make_plans_device", "lg_finalize_raw", "lg_np_cabs_host", "lg_np_pairwise_host", "lg_np_reduce_host",
     "lg_set_stream", "lg_set_timing", "lg_get_timing", "lg_bench_zgemm", "lg_device_count", "lg_last_error", "lg_version",
 )
@@ -102,6 +102,7 @@ def load() -> C.CDLL:
     lib.lg_eval_device.argtypes = [P, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.lg_plan_table.argtypes = [P, C.c_int64, C.c_double, dp, dp, i64p, i32p, i32p, dp, i64p, i32p, i32p]
     lib.lg_forward_states.argtypes = [P, C.c_int64, C.c_double, dp, dp]
+    lib.lg_step_derivative.argtypes = [P, C.c_int64, C.c_double, dp, C.c_int64, C.c_int32, dp, dp]
     lib.lg_raw_size.argtypes = [P, C.c_int64]
     lib.lg_raw_size.restype = C.c_int64
     lib.lg_raw_get.argtypes = [P, dp]

@@ -378,6 +378,19 @@ class NativeProblem:
                                                   _native.dptr(out.view(np.float64))))
         return out
 
+    def step_derivative(self, a: ControlField, step: int, channel: int, psi) -> np.ndarray:
+        """(dU_step/da_channel) psi of a DIAGONALIZATION problem from the device factorisation
+        (derivative_action_diag, src/derivatives.py:256-275)."""
+        amps = np.ascontiguousarray(a.amplitudes, np.float64)
+        vec = np.ascontiguousarray(psi, np.complex128)
+        if vec.shape != (self.dim,):
+            raise ValueError("state dimension mismatch")
+        out = np.zeros(self.dim, np.complex128)
+        _native.check(self._lib.lg_step_derivative(self.handle, a.n_steps, float(a.dt), _native.dptr(amps), int(step),
+                                                   int(channel), _native.dptr(vec.view(np.float64)),
+                                                   _native.dptr(out.view(np.float64))))
+        return out
+
     def plan_table(self, a: ControlField) -> dict:
         N, Kc = a.n_steps, a.n_channels
         amps = np.ascontiguousarray(a.amplitudes, np.float64)

@@ -700,6 +700,50 @@ int lg_forward_states(lg_problem* p, int64_t n_steps, double dt, const double* a
   return LG_OK;
 }
 
+// y = M x for one column-major d x d complex matrix (one CTA; rows over the threads)
+__global__ void lg_k_zgemv_one(const double2* __restrict__ M, const double2* __restrict__ x, int d, double2* __restrict__ y) {
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < d; ++j) {
+      const double2 m = M[(long)j * d + i], v = x[j];
+      acc.x += m.x * v.x - m.y * v.y;
+      acc.y += m.x * v.y + m.y * v.x;
+    }
+    y[i] = acc;
+  }
+}
+
+int lg_step_derivative(lg_problem* p, int64_t n_steps, double dt, const double* amps, int64_t step, int32_t channel,
+                       const double* psi, double* out) {
+  int rc = check_field(p, n_steps, dt, amps);
+  if (rc) return rc;
+  if (!psi || !out) return fail(LG_INVALID_ARG, "null state pointer");
+  if (p->backend != 1)
+    return fail(LG_UNSUPPORTED, "lg_step_derivative serves the DIAGONALIZATION backend (Taylor problems: lg_expm_apply "
+                                "on the embedded generator)");
+  if (step < 0 || step >= n_steps) return fail(LG_INDEX_ERROR, "step out of range");
+  if (channel < 0 || channel >= p->Kc) return fail(LG_INDEX_ERROR, "control channel out of range");
+  CK(cudaSetDevice(p->device));
+  rc = ensure_N(p, n_steps);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p->d_amps, amps, sizeof(double) * n_steps * p->Kc, cudaMemcpyHostToDevice, p->stream));
+  rc = prepare_steps(p, n_steps, dt, true);  // factorises every step and forms dU_n/da_k in p->d_D
+  if (rc) return rc;
+  const long d = p->d, dd = d * d;
+  double2* buf = nullptr;
+  CK(cudaMallocAsync(&buf, sizeof(double2) * 2 * d, p->stream));
+  cudaError_t e = cudaMemcpyAsync(buf, psi, sizeof(double2) * d, cudaMemcpyHostToDevice, p->stream);
+  if (e == cudaSuccess) {
+    lg_k_zgemv_one<<<1, 256, 0, p->stream>>>(p->d_D + ((long)step * p->Kc + channel) * dd, buf, (int)d, buf + d);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, buf + d, sizeof(double2) * d, cudaMemcpyDeviceToHost, p->stream);
+  cudaFreeAsync(buf, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) return fail(LG_CUDA_ERROR, std::string("lg_step_derivative: ") + cudaGetErrorString(e));
+  return LG_OK;
+}
+
 int lg_plan_table(lg_problem* p, int64_t n_steps, double dt, const double* amps, double* norm1, int64_t* sigma,
                   int32_t* order, int32_t* scaling, double* aux_arg, int64_t* aux_sigma, int32_t* aux_order,
                   int32_t* aux_scaling) {

@@ -11,10 +11,11 @@ two-norm surrogate sqrt(norm_1 norm_inf) and the embedding's sigma' for the deri
 materialised embedding up to 2 d = 256, the block operator's assembled bounds with its extra unit
 above, src/derivatives.py:133-196).  There is no host evaluation path.
 
-DIAGONALIZATION: ``forward`` / ``adjoint`` run a one-step device problem on that backend
-(hand-written Jacobi factorisation, csrc/lg_diag.cu); its derivative products exist only fused inside
-the device gradient (``composite_grad`` on a DIAGONALIZATION problem), so ``control_derivative``
-raises for that backend instead of falling back to the host.
+DIAGONALIZATION: ``forward`` / ``adjoint`` / ``control_derivative`` run a one-step device problem on
+that backend (hand-written Jacobi factorisation and the eigenbasis derivative formula of
+src/derivatives.py:256-275 in csrc/lg_diag.cu; the product through the C ABI's
+``lg_step_derivative``).  The host objects ``diag_prepare`` / ``DiagFactorization`` are not offered:
+the factorisation never leaves the device.
 """
 
 from __future__ import annotations
@@ -87,6 +88,16 @@ def _diag_action(ctx: StepContext, psi, sign: float) -> np.ndarray:
     ctrl = ctx.h_controls[0] if ctx.h_controls else build_csr([], d, d)
     problem = ControlProblem(ctx.h_step.scaled(sign), (ctrl,), ctx.backend, ctx.tau)
     return forward_propagate(problem, ControlField.constant(0.0, 1, 1, ctx.dt), _state(ctx, psi))
+
+
+def _diag_derivative(ctx: StepContext, channel: int, psi) -> np.ndarray:
+    """(dU/da_channel) psi on the device DIAGONALIZATION backend: the one-step problem H_n + 0 * h_c
+    (amplitudes already folded into h_step), product by lg_step_derivative."""
+    from .costs import ControlField, ControlProblem, NativeProblem
+
+    problem = ControlProblem(ctx.h_step, (ctx.h_controls[channel],), ctx.backend, ctx.tau)
+    npb = NativeProblem(problem, [], initial_states=_state(ctx, psi).reshape(1, -1))
+    return npb.step_derivative(ControlField.constant(0.0, 1, 1, ctx.dt), 0, 0, psi)
 
 
 def propagate(ctx: StepContext, psi) -> np.ndarray:
@@ -227,9 +238,7 @@ class StepEvaluator:
         if not 0 <= channel < len(self.ctx.h_controls):
             raise IndexError(f"control channel {channel} out of range")
         if self.ctx.backend is Backend.DIAGONALIZATION:
-            raise NotImplementedError(
-                "DIAGONALIZATION derivative products run only fused inside the device gradient "
-                "(composite_grad on a DIAGONALIZATION problem); there is no host evaluation path")
+            return _diag_derivative(self.ctx, channel, psi)
         if channel not in self._aux:
             gen, _ = self._generator_plan()
             matrix, bounds = _embedded(self.ctx, channel, gen)

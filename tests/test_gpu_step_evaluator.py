@@ -147,10 +147,54 @@ def test_block_operator_bounds_and_action_match_the_materialised_embedding(g):
     assert np.abs(u - ref[d:]).max() <= 1e-11
 
 
-def test_diagonalization_derivative_is_refused_not_computed_on_the_host(g):
-    ctx = StepContext(sparse.from_dense(_herm(g, 4)), (sparse.from_dense(_herm(g, 4)),), 0.2, Backend.DIAGONALIZATION)
+@pytest.mark.parametrize("d,tau", [(5, 1e-12), (40, 1e-12), (96, 1e-9)])
+def test_diagonalization_derivative_agrees_with_the_embedding_and_differences(g, d, tau):
+    # device eigenbasis formula (shared-memory Jacobi up to d = 64, global-memory Jacobi above) against
+    # the Taylor embedding and against central differences of the exact propagator
+    dt, a, eps = 0.3, 0.4, 1e-6
+    hs, hc, psi = _herm(g, d, 0.5), _herm(g, d, 0.5), _ket(g, d)
+    field = ControlField.constant(a, 1, 1, dt)
+    du = {}
+    for backend in (Backend.SCALING_SQUARING, Backend.DIAGONALIZATION):
+        # (tau = 1e-12 is infeasible for the dense d = 96 embedding, sigma' = 192: the Taylor planner
+        # raises PlanningError there exactly as the reference's does)
+        problem = ControlProblem(sparse.from_dense(hs), (sparse.from_dense(hc),), backend, tau)
+        du[backend] = problem.step_evaluator(field, 0).control_derivative(0, psi)
+    fd = (_exact(hs + (a + eps) * hc, dt, psi) - _exact(hs + (a - eps) * hc, dt, psi)) / (2 * eps)
+    assert np.linalg.norm(du[Backend.DIAGONALIZATION] - du[Backend.SCALING_SQUARING]) <= 10 * tau + 1e-9 * np.linalg.norm(fd)
+    assert np.linalg.norm(du[Backend.DIAGONALIZATION] - fd) <= 1e-6 * np.linalg.norm(fd)
+
+
+def test_diagonalization_derivative_with_a_degenerate_static_spectrum(g):
+    # H_s has a doubly degenerate level; the driven step generator stays finite and matches differences
+    # (the divided-difference weights switch to the diagonal term below the 1e-12 max|w| gap rule,
+    # src/derivatives.py:45,237)
+    h0 = np.diag([1.0, 1.0, 2.0]).astype(complex)
+    hc, psi = _herm(g, 3), _ket(g, 3)
+    a, dt, eps = 0.17, 0.6, 1e-6
+    problem = ControlProblem(sparse.from_dense(h0), (sparse.from_dense(hc),), Backend.DIAGONALIZATION, 1e-12)
+    du = problem.step_evaluator(ControlField.constant(a, 1, 1, dt), 0).control_derivative(0, psi)
+    assert np.isfinite(du).all()
+    fd = (_exact(h0 + (a + eps) * hc, dt, psi) - _exact(h0 + (a - eps) * hc, dt, psi)) / (2 * eps)
+    assert np.linalg.norm(du - fd) <= 1e-6 * np.linalg.norm(fd)
+
+
+def test_step_derivative_abi_rejects_taylor_problems_and_bad_indices(g):
+    from paper_2304_06200_b200.costs import NativeProblem
+
+    d = 4
+    hs, hc, psi = _herm(g, d), _herm(g, d), _ket(g, d)
+    field = ControlField.constant(0.1, 2, 1, 0.2)
+    taylor = NativeProblem(ControlProblem(sparse.from_dense(hs), (sparse.from_dense(hc),)), [], initial_states=psi)
     with pytest.raises(NotImplementedError):
-        StepEvaluator(ctx).control_derivative(0, _ket(g, 4))
+        taylor.step_derivative(field, 0, 0, psi)
+    diag = NativeProblem(ControlProblem(sparse.from_dense(hs), (sparse.from_dense(hc),), Backend.DIAGONALIZATION), [],
+                         initial_states=psi)
+    with pytest.raises(IndexError):
+        diag.step_derivative(field, 2, 0, psi)
+    with pytest.raises(IndexError):
+        diag.step_derivative(field, 0, 1, psi)
+    assert diag.step_derivative(field, 1, 0, psi).shape == (d,)
 
 
 def test_stepwise_forward_equals_the_sweep_and_rebuilds_the_gradient(g):
