@@ -139,11 +139,35 @@ int dense_aux_chain(lg_problem* p, int T, const int* gch, int G, int m, int s, c
   double2* bufs[2] = {p->dd_xtb0, p->dd_xtb1};
   const double2* prev = nullptr;
   int b = 0;
+  // Narrow chains (a small shard of the K-state block: T <= LG_AUX_MERGE columns, default 8) are bound by
+  // streaming the d x d operators from HBM, not by the MMAs: a single-channel chain then runs tops and
+  // bottoms as ONE two-segment GEMM per term (2 operator reads instead of 3, full 16-column tiles).
+  // The T columns behind the bottoms of both term buffers are zeroed per chain (another trajectory set
+  // or channel group may have used them).
+  static const int merge_T = [] {
+    const char* e = std::getenv("LG_AUX_MERGE");
+    return e ? std::atoi(e) : 8;
+  }();
+  const bool merged = G == 1 && T <= merge_T && m * s > 1;
+  if (merged)
+    for (double2* tb : bufs)
+      CK(cudaMemsetAsync(tb + 2L * T * d, 0, sizeof(double2) * (size_t)T * d, p->stream));
   for (int si = 0; si < s; ++si)
     for (int j = 1; j <= m; ++j) {
       const bool first = si == 0 && j == 1, last = j == m;
       const double r = 1.0 / (double)(s * j);
       double2* out = bufs[b];
+      if (merged && !first) {
+        // one pass [A | A_c] [[X_top, X_bot], [X_bot, 0]] over the 2 T columns [top | bottom]: A and A_c are
+        // each read once per term instead of A twice and A_c once (the zero columns behind the bottoms
+        // add exact zeros)
+        int rc = dense_gemm(p, p->d_Ad, prev, p->d_Acd[gch[0]], prev + (long)T * d, 2 * T, r, false, last, nullptr,
+                            p->dd_xcur, out);
+        if (rc) return rc;
+        prev = out;
+        b ^= 1;
+        continue;
+      }
       for (int gi = 0; gi < G; ++gi) {
         const int k = gch[gi];
         int rc;
@@ -247,7 +271,8 @@ int configure_dense(lg_problem* p) {
     const int lo = (int)std::min<long>(p->shard_b, p->set_T[s]), hi = (int)std::min<long>(p->shard_e, p->set_T[s]);
     Tmax = std::max(Tmax, hi - lo);
   }
-  const long cst = (long)Tmax * (1 + Imax), cx = (long)(p->Kc + 1) * Tmax;
+  // aux term buffers: K_c T tops + T bottoms + T columns that stay zero (merged aux pass, dense_aux_chain)
+  const long cst = (long)Tmax * (1 + Imax), cx = (long)(p->Kc + 2) * Tmax;
   DevMem& M = p->mem;
   p->d_Ad = M.alloc<double2>((size_t)d * d);
   p->d_Acd.assign(p->Kc, nullptr);
