@@ -174,6 +174,19 @@ def committed_traffic(workload, kernel, n_steps):
     return None, None
 
 
+def committed_smem_wavefronts(workload, kernel, n_steps):
+    """Shared-memory wavefronts per launch of the dominant kernel from the same committed capture
+    (profiles/r02_traffic.json: l1tex__data_pipe_lsu_wavefronts_mem_shared.sum), scaled to n_steps."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
+            t = json.load(fh).get(workload)
+    except Exception:
+        return None
+    if not t or t["kernel"] not in kernel or "smem_wavefronts_per_launch" not in t:
+        return None
+    return t["smem_wavefronts_per_launch"] * n_steps / t["n_steps_captured"]
+
+
 def critical_path_terms(plan_table):
     """Sequentially dependent operator-terms of one evaluation: the forward chain
     N*mu, then per backward step the adjoint chain mu plus the aux chain mu_aux (channels sharing a
@@ -476,6 +489,17 @@ def run_ours(args):
     e2e_value = jobs * e2e_steps / (float(te.item()) / 1e3)
 
     roofline = run.roofline(phase, nevals, traffic_ok=(mode != "shard"))
+    clocks = clk.summary()
+    wf = committed_smem_wavefronts(case.name, roofline["kernel"], N) if mode != "shard" else None
+    if wf and clocks.get("sm_mhz"):
+        # what actually bounds the sparse cluster kernels (state windows live in shared memory): the
+        # shared-memory pipe, 1 wavefront per cycle per SM, over all SMs of the device at the clock
+        # sampled during the timed region; wavefront count from the committed ncu capture
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        per_clk = wf / ((phase[2] / nevals / 1e3) * clocks["sm_mhz"] * 1e6 * sms)
+        roofline["onchip"] = {"bound": "shared-memory pipe", "wavefronts_per_launch": wf, "sms": sms,
+                              "achieved": per_clk, "peak": 1.0, "unit": "wavefronts/clk/SM", "frac": per_clk,
+                              "source": "profiles/r02_c4_final_ncu.md"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -489,7 +513,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N * Kc,
                 "d2h_bytes_per_step": 8 * N * Kc + 8, "steps": e2e_steps},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "cost": res.cost,
     }
     if mode == "shard":
