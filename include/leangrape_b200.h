@@ -166,6 +166,11 @@ int lg_expm_plan_inputs(const lg_matrix* a, double* norm1, int64_t* sigma_prime)
 int lg_expm_apply(const lg_matrix* a, int64_t n_vec, const double* psi, int32_t order, int32_t scaling,
                   double* out, int32_t device);
 
+/* y_k = A x_k for n_vec vectors [n_vec][2 n] on the device (CsrMatrix.matvec / DenseMatrix.matvec /
+ * sparse.matvec, src/sparse.py:69-88,193-199,297-298): the stored matrix goes through the same ELL
+ * layout and row kernel the sweeps use for penalty operators. */
+int lg_matvec(const lg_matrix* a, int64_t n_vec, const double* x, double* y, int32_t device);
+
 /* make_plan (src/expm.py:279-303) on the host: bit-identical to the reference. */
 int lg_make_plan(double norm1, int64_t sigma_prime, double tau, int32_t m_max, int32_t s_max, int32_t* order,
                  int32_t* scaling, double* bound);

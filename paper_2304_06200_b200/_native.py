@@ -26,7 +26,7 @@ LG_UNSUPPORTED = 6
 
 EXPORTED = (
     "lg_problem_create", "lg_problem_destroy", "lg_eval", "lg_cost", "lg_cost_batch", "lg_eval_device", "lg_plan_table",
-    "lg_forward_states", "lg_step_derivative", "lg_raw_size", "lg_raw_get", "lg_finalize_host", "lg_make_plan",
+    "lg_forward_states", "lg_step_derivative", "lg_matvec", "lg_raw_size", "lg_raw_get", "lg_finalize_host", "lg_make_plan",
     "lg_make_plans_device", "lg_finalize_raw", "lg_np_cabs_host", "lg_np_pairwise_host", "lg_np_reduce_host",
     "lg_set_stream", "lg_set_timing", "lg_get_timing", "lg_bench_zgemm", "lg_device_count", "lg_last_error", "lg_version",
 )
@@ -110,6 +110,7 @@ def load() -> C.CDLL:
     lib.lg_set_raw_buffer.argtypes = [P, C.c_void_p, C.c_int64]
     lib.lg_expm_plan_inputs.argtypes = [C.POINTER(lg_matrix), dp, i64p]
     lib.lg_expm_apply.argtypes = [C.POINTER(lg_matrix), C.c_int64, dp, C.c_int32, C.c_int32, dp, C.c_int32]
+    lib.lg_matvec.argtypes = [C.POINTER(lg_matrix), C.c_int64, dp, dp, C.c_int32]
     lib.lg_eval_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp, dp]
     lib.lg_cost_sharded.argtypes = [P, C.c_int64, C.c_double, dp, ALLREDUCE_FN, C.c_void_p, dp]
     lib.lg_make_plan.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_int32, C.c_int32, i32p, i32p, dp]

@@ -924,6 +924,52 @@ int lg_expm_apply(const lg_matrix* a, int64_t n_vec, const double* psi, int32_t 
   return rc;
 }
 
+int lg_matvec(const lg_matrix* a, int64_t n_vec, const double* x, double* y, int32_t device) {
+  if (!a || !x || !y || n_vec < 1) return fail(LG_INVALID_ARG, "bad arguments");
+  Mat m;
+  int rc = parse_mat(*a, a->n, &m, "matrix");
+  if (rc) return rc;
+  const long d = m.n;
+  if (d < 1) return fail(LG_INVALID_ARG, "empty matrix");
+  int W = 1;
+  std::vector<int> cols;
+  std::vector<double2> vals;
+  to_ell(m, &W, cols, vals, nullptr);
+  CK(cudaSetDevice(device));
+  DevMem mem;
+  const int* dcols = mem.upload(cols);
+  const double2* dvals = mem.upload(vals);
+  std::vector<double2> h((size_t)d * n_vec);
+  std::memcpy(h.data(), x, sizeof(double2) * h.size());
+  const double2* dx = mem.upload(h);
+  double2* dy = mem.alloc<double2>(h.size());
+  if (!dcols || !dvals || !dx || !dy) return fail(LG_CUDA_ERROR, "device allocation failed");
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (int64_t b0 = 0; b0 < n_vec && rc == LG_OK; b0 += 64) {
+    LgEllArgs A{};
+    A.d = (int)d;
+    A.W = W;
+    A.ncol = (int)std::min<int64_t>(64, n_vec - b0);
+    A.accumulate = 0;
+    A.cols = dcols;
+    A.vals = dvals;
+    for (int q = 0; q < A.ncol; ++q) {
+      A.x[q] = dx + (b0 + q) * d;
+      A.y[q] = dy + (b0 + q) * d;
+    }
+    void* args[] = {&A};
+    rc = launch(lg_ell_kernel(), dim3((unsigned)((d + 255) / 256), (unsigned)A.ncol), dim3(256), args, 0, st);
+  }
+  if (rc == LG_OK) {
+    cudaMemcpyAsync(y, dy, sizeof(double2) * h.size(), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(LG_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  cudaStreamDestroy(st);
+  return rc;
+}
+
 int lg_finalize_host(lg_problem* p, int64_t N, const double* raw, double* cost, double* grad) {
   const long S = (long)p->specs.size(), T = p->T_total, Kc = p->Kc;
   const double2* ip = (const double2*)raw;

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import expm
 from .costs import Backend
-from .sparse import DenseMatrix, as_own_matrix, build_csr, build_csr_arrays, is_hermitian, to_dense
+from .sparse import DenseMatrix, as_own_matrix, aux_embed, build_csr, build_csr_arrays, is_hermitian, to_dense
 
 __all__ = ["Backend", "StepContext", "BlockDerivativeOperator", "StepEvaluator", "propagate", "propagate_adjoint",
            "aux_embed", "aux_plan", "derivative_action_aux", "MATERIALIZE_DIM_LIMIT"]
@@ -114,26 +114,6 @@ def propagate_adjoint(ctx: StepContext, psi) -> np.ndarray:
         return _diag_action(ctx, psi, -1.0)
     gen = _generator(ctx)
     return expm.apply(gen.scaled(-1.0), _state(ctx, psi), _plan_for(ctx, gen), validate=False)
-
-
-def aux_embed(h_step, h_control, dt: float):
-    """[[-i dt H, -i dt h_c], [0, -i dt H]] as a stored matrix (src/sparse.py:352-380): dense when
-    either block is dense, CSR otherwise, entries scaled by -i dt in one multiplication each."""
-    h_step, h_control = as_own_matrix(h_step), as_own_matrix(h_control)
-    d = h_step.shape[0]
-    if h_step.shape != h_control.shape or h_step.shape[1] != d:
-        raise ValueError("aux_embed expects two square matrices of equal dimension")
-    scale = -1j * dt
-    if isinstance(h_step, DenseMatrix) or isinstance(h_control, DenseMatrix):
-        big = np.zeros((2 * d, 2 * d), np.complex128, order="F")
-        big[:d, :d] = scale * to_dense(h_step)
-        big[:d, d:] = scale * to_dense(h_control)
-        big[d:, d:] = big[:d, :d]
-        return DenseMatrix(big)
-    hr, hc, hv = h_step.triplets()
-    cr, cc, cv = h_control.triplets()
-    return build_csr_arrays(np.concatenate([hr, cr, hr + d]), np.concatenate([hc, cc + d, hc + d]),
-                            scale * np.concatenate([hv, cv, hv]), 2 * d, 2 * d)
 
 
 class BlockDerivativeOperator:

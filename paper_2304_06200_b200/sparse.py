@@ -28,6 +28,12 @@ __all__ = [
     "from_dense",
     "identity_csr",
     "linear_combine",
+    "matvec",
+    "one_norm",
+    "inf_norm",
+    "max_row_nnz",
+    "aux_embed",
+    "is_anti_hermitian",
     "kron_csr",
     "is_hermitian",
     "to_dense",
@@ -99,9 +105,8 @@ class CsrMatrix:
         return CsrMatrix(self.n_rows, self.n_cols, self.row_offsets, self.col_indices, self.values * complex(factor))
 
     def matvec(self, v, out=None):
-        raise NotImplementedError(
-            "CsrMatrix.matvec: the product runs matvecs only fused inside the GPU sweeps "
-            "(composite_grad / composite_cost / expm.apply); there is no host matvec (no CPU fallback)")
+        """A v on the GPU (src/sparse.py:69-88); there is no host matvec."""
+        return matvec(self, v, out)
 
     def triplets(self):
         rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_offsets))
@@ -169,9 +174,8 @@ class DenseMatrix:
         return DenseMatrix(self.array * complex(factor))
 
     def matvec(self, v, out=None):
-        raise NotImplementedError(
-            "DenseMatrix.matvec: the product runs matvecs only fused inside the GPU sweeps "
-            "(composite_grad / composite_cost / expm.apply); there is no host matvec (no CPU fallback)")
+        """A v on the GPU (src/sparse.py:193-199); there is no host matvec."""
+        return matvec(self, v, out)
 
     def to_dense(self) -> np.ndarray:
         return self.array.copy(order="F")
@@ -263,6 +267,80 @@ def linear_combine(coeffs, mats):
     if not rs:
         return build_csr([], *shape)
     return build_csr_arrays(np.concatenate(rs), np.concatenate(cs), np.concatenate(vs), *shape)
+
+
+def matvec(m, v, out=None):
+    """A v (or A applied to every row of a (K, n) block) evaluated on the GPU through the C ABI's
+    ``lg_matvec`` -- the ELL row kernel of the sweeps; mirrors ``sparse.matvec`` / ``CsrMatrix.matvec`` /
+    ``DenseMatrix.matvec`` (src/sparse.py:69-88,193-199,297-298).  Square matrices (the library's
+    descriptor); raises without the library or a GPU -- there is no host product."""
+    import ctypes as C
+
+    from . import _native
+    from .costs import _Keep, _matrix
+
+    m = as_own_matrix(m)
+    n_rows, n_cols = m.shape
+    x = np.asarray(v, dtype=np.complex128)
+    if x.ndim not in (1, 2) or x.shape[-1] != n_cols:
+        raise SparseMatrixError("matvec dimension mismatch")
+    if n_rows != n_cols:
+        raise NotImplementedError("device matvec serves square matrices (lg_matrix)")
+    rows = np.ascontiguousarray(x.reshape(-1, n_cols))
+    res = np.empty_like(rows)
+    keep = _Keep()
+    desc = _matrix(m, n_rows, keep)
+    _native.check(_native.load().lg_matvec(C.byref(desc), rows.shape[0], _native.dptr(rows.view(np.float64)),
+                                           _native.dptr(res.view(np.float64)), 0))
+    res = res.reshape(x.shape)
+    if out is not None:
+        if out.shape != res.shape:
+            raise SparseMatrixError("out has the wrong shape")
+        np.copyto(out, res)
+        return out
+    return res
+
+
+def one_norm(m) -> float:
+    """Module-level accessors of the reference (src/sparse.py:301-310)."""
+    return as_own_matrix(m).one_norm()
+
+
+def inf_norm(m) -> float:
+    return as_own_matrix(m).inf_norm()
+
+
+def max_row_nnz(m) -> int:
+    return as_own_matrix(m).max_row_nnz()
+
+
+def aux_embed(h_step, h_control, dt: float):
+    """[[-i dt H, -i dt h_c], [0, -i dt H]] as a stored matrix (src/sparse.py:352-380): dense when
+    either block is dense, CSR otherwise, entries scaled by -i dt in one multiplication each."""
+    h_step, h_control = as_own_matrix(h_step), as_own_matrix(h_control)
+    d = h_step.shape[0]
+    if h_step.shape != h_control.shape or h_step.shape[1] != d:
+        raise SparseMatrixError("aux_embed expects two square matrices of equal dimension")
+    scale = -1j * dt
+    if isinstance(h_step, DenseMatrix) or isinstance(h_control, DenseMatrix):
+        big = np.zeros((2 * d, 2 * d), np.complex128, order="F")
+        big[:d, :d] = scale * to_dense(h_step)
+        big[:d, d:] = scale * to_dense(h_control)
+        big[d:, d:] = big[:d, :d]
+        return DenseMatrix(big)
+    hr, hc, hv = h_step.triplets()
+    cr, cc, cv = h_control.triplets()
+    return build_csr_arrays(np.concatenate([hr, cr, hr + d]), np.concatenate([hc, cc + d, hc + d]),
+                            scale * np.concatenate([hv, cv, hv]), 2 * d, 2 * d)
+
+
+def is_anti_hermitian(m, tol: float) -> bool:
+    """max |M + M^dagger| <= tol (src/sparse.py:400-404)."""
+    m = as_own_matrix(m)
+    if m.shape[0] != m.shape[1]:
+        return False
+    dense = to_dense(m)
+    return float(np.max(np.abs(dense + dense.conj().T), initial=0.0)) <= tol
 
 
 def kron_csr(a: CsrMatrix, b: CsrMatrix) -> CsrMatrix:
