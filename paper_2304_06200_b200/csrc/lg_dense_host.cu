@@ -30,8 +30,10 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
   // C = 64: 22.6 (1 slice) -> 29.7 TF/s (4); C = 128: 25.8 -> 31.2 TF/s (4) (tools/bench_zgemm.py).
   // wide tile (4 warps of 16 x 32) from 64 columns: half the A-fragment loads per DMMA
   // (tools/bench_zgemm.py, d = 4096: C = 64 33.0 -> 34.3, C = 128 35.0 -> 35.9 TF/s, split-k 8)
+  // ... and from 32 columns since the bulk-copy kernel: d = 4096, C = 32: 0.155 ms with the 16 x 16 warp
+  // tiles, 0.120 ms with the bulk kernel's 16 x 32 (36.0 TF/s; a shard of 32 trajectories)
   const char* ev = std::getenv("LG_ZGEMM_N32");
-  const int n32_from = ev ? std::atoi(ev) : 64;
+  const int n32_from = ev ? std::atoi(ev) : 32;
   const int ntt = n32_from > 0 && C >= n32_from ? 4 : 2;
   const int bn = 8 * ntt;
   int smem = lg_zgemm_smem_bytes(ntt);
@@ -40,21 +42,28 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
   // 4-stage mbarrier ring (producer warp + 4 MMA warps); LG_ZGEMM_BULK=0 keeps the cp.async kernel
   const char* eb = std::getenv("LG_ZGEMM_BULK");
   const bool bulk_on = !(eb && std::atoi(eb) == 0);
-  const bool bulk = bulk_on && ntt == 4 && d % 64 == 0 && C % 32 == 0;  // every segment has K = lda = d
+  // (every segment has K = lda = d); the 16-column variant serves narrow chains (LG_ZGEMM_BULK16=0: off)
+  const char* eb16 = std::getenv("LG_ZGEMM_BULK16");
+  const bool bulk = bulk_on && d % 64 == 0 && C % bn == 0 && (ntt == 4 || !(eb16 && std::atoi(eb16) == 0));
   int threads = 128;
   if (bulk) {
-    kern = lg_zgemm_bulk_kernel();
-    smem = lg_zgemm_bulk_smem_bytes();
+    kern = lg_zgemm_bulk_kernel(ntt);
+    smem = lg_zgemm_bulk_smem_bytes(ntt);
     threads = 160;
   }
   // (launch() raises the kernel's dynamic shared-memory limit to `smem` when it exceeds 48 KB)
   const long nct = (long)((C + bn - 1) / bn) * ((d + 63) / 64);
-  int ks = (int)std::max<long>(1, std::min<long>(ntt == 4 ? 8 : 4, 2048L / std::max<long>(nct, 1)));
+  // narrow chains (8 - 16 columns: small shards) stream the operator from HBM for little arithmetic: more
+  // k-slices keep more copies in flight (d = 4096, C = 8 / 16: 0.082 / 0.085 ms with 4 slices, 0.073 /
+  // 0.076 ms with 16, 0.079 / 0.084 ms with 32; tools/bench_zgemm.py)
+  const long ktiles = (long)((d + 15) / 16) * (B ? 2 : 1);
+  int ks = (int)std::max<long>(1, std::min<long>({ntt == 4 ? 8L : 16L, 2048L / std::max<long>(nct, 1), ktiles}));
   if (bulk) {
     // the k-slices that fill whole waves of co-resident CTAs: minimise waves x (k-tiles per slice + ~2
     // tiles of pipeline fill and epilogue); d = 4096: C = 64 -> 9 slices (37.1 vs 35.1 TF/s with 8),
     // C = 128 -> 8 (LG_SPLITK sweep, tools/bench_zgemm.py)
-    static int slots = 0;
+    static int slots_of[2] = {0, 0};
+    int& slots = slots_of[ntt == 4];
     if (!slots) {
       int dev = 0, sms = 148, occ = 2;
       cudaGetDevice(&dev);

@@ -1,4 +1,7 @@
-"""Time the c5 operator-term kernel (DMMA complex GEMM + fused Taylor epilogue)."""
+"""Time the c5 operator-term kernel (DMMA complex GEMM + fused Taylor epilogue).
+
+    python tools/bench_zgemm.py [columns ...]      (default 64 128)
+"""
 import ctypes as C
 import json
 import os
@@ -9,7 +12,7 @@ from paper_2304_06200_b200 import _native  # noqa: E402
 
 lib = _native.load()
 out = {}
-for c in (64, 128):
+for c in ([int(a) for a in sys.argv[1:]] or [64, 128]):
     ms = C.c_double()
     _native.check(lib.lg_bench_zgemm(4096, c, 20, C.byref(ms)))
     out[f"lg_zgemm_4096x{c}_ms"] = ms.value
