@@ -430,17 +430,10 @@ constexpr int LG_ZG_STAGES = 4;
 extern "C" __global__ void __launch_bounds__(160) lg_k_zgemm_taylor_bulk(const __grid_constant__ LgGemmArgs G) {
   zgemm_taylor_bulk<4, LG_ZG_STAGES>(G);
 }
-// 16-column variant (16 x 16 warp tiles) for narrow chains: the same ring keeps 4 operator stages per
-// CTA in flight, which is what an HBM-bound 8 - 16 column term needs
-extern "C" __global__ void __launch_bounds__(160) lg_k_zgemm_taylor_bulk16(const __grid_constant__ LgGemmArgs G) {
-  zgemm_taylor_bulk<2, LG_ZG_STAGES>(G);
+extern "C" int lg_zgemm_bulk_smem_bytes() {
+  return (int)(sizeof(double2) * LG_ZG_STAGES * (BK * SAM + 32 * SXK) + 2 * LG_ZG_STAGES * sizeof(unsigned long long));
 }
-extern "C" int lg_zgemm_bulk_smem_bytes(int ntt) {
-  return (int)(sizeof(double2) * LG_ZG_STAGES * (BK * SAM + 8 * ntt * SXK) + 2 * LG_ZG_STAGES * sizeof(unsigned long long));
-}
-extern "C" void* lg_zgemm_bulk_kernel(int ntt) {
-  return ntt == 4 ? (void*)lg_k_zgemm_taylor_bulk : (void*)lg_k_zgemm_taylor_bulk16;
-}
+extern "C" void* lg_zgemm_bulk_kernel() { return (void*)lg_k_zgemm_taylor_bulk; }
 
 // Split-k finish: y = sum of the k-slices in slice order (deterministic), then the Taylor update.
 extern "C" __global__ void lg_k_taylor_epi(const __grid_constant__ LgGemmArgs G) {

@@ -42,13 +42,11 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
   // 4-stage mbarrier ring (producer warp + 4 MMA warps); LG_ZGEMM_BULK=0 keeps the cp.async kernel
   const char* eb = std::getenv("LG_ZGEMM_BULK");
   const bool bulk_on = !(eb && std::atoi(eb) == 0);
-  // (every segment has K = lda = d); the 16-column variant serves narrow chains (LG_ZGEMM_BULK16=0: off)
-  const char* eb16 = std::getenv("LG_ZGEMM_BULK16");
-  const bool bulk = bulk_on && d % 64 == 0 && C % bn == 0 && (ntt == 4 || !(eb16 && std::atoi(eb16) == 0));
+  const bool bulk = bulk_on && ntt == 4 && d % 64 == 0 && C % 32 == 0;  // every segment has K = lda = d
   int threads = 128;
   if (bulk) {
-    kern = lg_zgemm_bulk_kernel(ntt);
-    smem = lg_zgemm_bulk_smem_bytes(ntt);
+    kern = lg_zgemm_bulk_kernel();
+    smem = lg_zgemm_bulk_smem_bytes();
     threads = 160;
   }
   // (launch() raises the kernel's dynamic shared-memory limit to `smem` when it exceeds 48 KB)
@@ -62,8 +60,7 @@ int dense_gemm(lg_problem* p, const double2* A, const double2* X, const double2*
     // the k-slices that fill whole waves of co-resident CTAs: minimise waves x (k-tiles per slice + ~2
     // tiles of pipeline fill and epilogue); d = 4096: C = 64 -> 9 slices (37.1 vs 35.1 TF/s with 8),
     // C = 128 -> 8 (LG_SPLITK sweep, tools/bench_zgemm.py)
-    static int slots_of[2] = {0, 0};
-    int& slots = slots_of[ntt == 4];
+    static int slots = 0;
     if (!slots) {
       int dev = 0, sms = 148, occ = 2;
       cudaGetDevice(&dev);

@@ -33,8 +33,8 @@ extern "C" void* lg_cta_kernel(int backward, int maxr, int maxc, int wreg);
 extern "C" void* lg_zgemm_kernel();
 extern "C" void* lg_zgemm_n32_kernel();
 extern "C" int lg_zgemm_smem_bytes(int ntt);
-extern "C" void* lg_zgemm_bulk_kernel(int ntt);
-extern "C" int lg_zgemm_bulk_smem_bytes(int ntt);
+extern "C" void* lg_zgemm_bulk_kernel();
+extern "C" int lg_zgemm_bulk_smem_bytes();
 extern "C" void* lg_taylor_epi_kernel();
 extern "C" void* lg_cl_kernel(int backward, int W, int maxc, int small);
 extern "C" int lg_cl_smem_words(int R, int H, int Q, int E, int cmax, int W, int acw);
