@@ -193,7 +193,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
           void* iargs[] = {&Ei};
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(clusters * p->cli_CS);
-          cfg.blockDim = dim3(320);
+          cfg.blockDim = dim3(p->cli_T);
           cfg.dynamicSmemBytes = p->cli_smem;
           cfg.stream = st ? st : p->stream;
           cudaLaunchAttribute at[1];

@@ -4,6 +4,13 @@
 
 namespace lgi {
 
+// thread count of the LARGE cluster kernels (lg_sweep_cl_large.cuh: __launch_bounds__(384))
+static int cll_threads() {
+  const char* e = std::getenv("LG_CLL_T");
+  const int t = e ? std::atoi(e) : 320;
+  return t >= 64 && t <= 384 && t % 32 == 0 ? t : 320;
+}
+
 // Reverse Cuthill-McKee renumbering of a symmetric pattern (rows -> neighbour lists).
 std::vector<int> rcm_order(long d, const std::vector<std::vector<int>>& adj) {
   std::vector<int> order;
@@ -259,7 +266,10 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   // three rows per thread at 224 threads (255 registers, 7 warps): 108.8 / 795.3 ms.
   int threads = 32 * ((R + 2 * E + 31) / 32);
   const bool force_large = std::getenv("LG_CL_LARGE") && std::atoi(std::getenv("LG_CL_LARGE")) == 1;
-  const int rpt = 2, LT = 320, lsm = 3;
+  // LG_CLL_T=384 (A/B knob): 12 warps = 3 per SM sub-partition instead of 10 warps loading them
+  // 3 / 3 / 2 / 2.  Measured neutral (c4 N' = 400: 791.8 vs 791.5 ms; c3 96.8 vs 97.3 ms): the terms are
+  // paced by the SM-wide shared-memory pipe, not by the fullest sub-partition.
+  const int rpt = 2, LT = cll_threads(), lsm = 3;
   if ((!small || force_large) && Q == 1 && p->Wc <= 2 && R <= rpt * LT && !std::getenv("LG_CL_NOLARGE")) {
     const int cstl = cmax | 1;
     const int wf = lg_cll_mb_word(R, H, LT, cstl, 0, rpt) + 1, wbl = lg_cll_mb_word(R, H, LT, cstl, p->Kc * 2, rpt) + 1;
@@ -375,7 +385,7 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   if (p->cl_aux_ncl > 0 && small != 3 && p->Wc <= 2 && !std::getenv("LG_CL_NOITEMLAYOUT")) {
     void* fi = lg_cl_kernel(5, p->W, maxc, 3);
     for (int cs = 2; cs <= 8 && fi; cs *= 2) {
-      const int Ri = (int)((d + cs - 1) / cs), LT = 320, cstl = cmax | 1;
+      const int Ri = (int)((d + cs - 1) / cs), LT = cll_threads(), cstl = cmax | 1;
       if (Ri > 2 * LT || Ri < H || 16L * cstl * (Ri + 2 * H) >= 65536) continue;
       const int wbl = lg_cll_mb_word(Ri, H, LT, cstl, p->Kc * 2, 2) + 1;
       if ((long)wbl * 16 > cap || cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, wbl * 16) != cudaSuccess)
@@ -398,6 +408,7 @@ bool configure_cl(lg_problem* p, int smem_optin) {
       }
       if (ncl < 1) continue;
       p->cli_CS = cs;
+      p->cli_T = LT;
       p->cli_R = Ri;
       p->cli_smem = wbl * 16;
       p->cli_ncl = ncl;

@@ -167,7 +167,7 @@ struct lg_problem {
   unsigned cl_cshare = 0;  // bit k: control channel k has channel k-1's (renumbered) column pattern
   int cl_aux_ncl = 0;  // two-phase backward: co-resident clusters of the item kernel (0: fused backward)
   // item layout: the derivative-product items on smaller clusters of the LARGE kernels (0: the sweep layout)
-  int cli_CS = 0, cli_R = 0, cli_smem = 0, cli_ncl = 0;
+  int cli_CS = 0, cli_R = 0, cli_smem = 0, cli_ncl = 0, cli_T = 320;
   DevMem bkmem;        // ... its psi_{n-1} / lambda_s(n) store
   long bk_cap = 0;
   double2 *d_bk_psi = nullptr, *d_bk_lam = nullptr;

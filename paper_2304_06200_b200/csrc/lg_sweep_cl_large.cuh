@@ -25,13 +25,16 @@
 #pragma once
 
 // RPT rows per thread at the thread count that gives the register budget they need (R <= RPT T):
-// RPT 2 -> 320 threads (10 warps, 168 registers), RPT 3 -> 224 threads (7 warps, 255 registers)
-#define CLL_T(RPT) ((RPT) == 2 ? 320 : 224)
+// RPT 2 -> up to 384 threads (12 warps = 3 per SM sub-partition, 168 registers: the register file is
+// split per sub-partition, so 10 warps have the same budget but load the sub-partitions 3 / 3 / 2 / 2),
+// RPT 3 -> 224 threads (7 warps, 255 registers).  The host launches LG_CLL_T threads (default 320; 384
+// measured neutral).
+#define CLL_T(RPT) ((RPT) == 2 ? 384 : 224)
 
 namespace {
 
 struct ClL {
-  int d, R, H, WIN, CST, rank, CS, T, g0, Wc, dbg;  // window rows WIN, column stride CST (odd)
+  int d, R, H, WIN, CST, rank, CS, T, AS, g0, Wc, dbg;  // window rows WIN, column stride CST (odd), staged-row stride AS
   int red, rt, tb0, tb1, acs, accs, mb;
   mutable unsigned ph;  // parity bits of the next phase of the two exchange mbarriers
   const int* perm;      // renumbered row -> original row
@@ -77,9 +80,10 @@ __device__ __forceinline__ ClL make_cll(const LgEngineArgs& E, int cmax, bool st
   c.tb1 = o;
   o += c.CST * c.WIN;
   c.acs = c.accs = -1;
+  c.AS = lg_cll_as(c.R, c.T, RPT);
   if (stage_ac) {
     c.acs = o;
-    o += E.Kc * 2 * RPT * c.T;
+    o += E.Kc * 2 * c.AS;
     c.accs = o;
   }
   c.mb = lg_cll_mb_word(c.R, c.H, c.T, c.CST, stage_ac ? E.Kc * 2 : 0, RPT);
@@ -183,6 +187,7 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
   const char* xbuf = reinterpret_cast<const char*>(cl_sm + X);
 #pragma unroll
   for (int rr = 0; rr < RPT; ++rr) {
+    if (!c.slot(rr)) continue;  // thread slots past the CTA's rows (whole warps of them at 384 threads)
     // FMA chains per column: four (a.x x and a.y (i x) apart) for one or two columns, two for
     // wider terms, whose columns give enough independent chains (and need the registers)
     constexpr bool SPL = NC <= 2;
@@ -203,7 +208,7 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
         const int koff = tab[q];
         double2 xb[2];
         {
-          const int o0 = accb[koff], o1 = accb[koff + RPT * c.T];
+          const int o0 = accb[koff], o1 = accb[koff + c.AS];
           xb[0] = cl_sm[widx(c, X, o0, NC - 1)];
           xb[1] = cl_sm[widx(c, X, o1, NC - 1)];
         }
@@ -211,7 +216,7 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
         for (int h = 0; h < STEP; ++h) {
           const double2* ac = cl_sm + c.acs + tab[q + h] + c.lr(rr);
           cmac(p[q + h], pq[SPL ? q + h : 0], ac[0], xb[0], SPL);
-          cmac(p[q + h], pq[SPL ? q + h : 0], ac[RPT * c.T], xb[1], SPL);
+          cmac(p[q + h], pq[SPL ? q + h : 0], ac[c.AS], xb[1], SPL);
         }
       }
     }
@@ -431,7 +436,7 @@ __device__ __forceinline__ void aux_products_l(const LgEngineArgs& E, const ClL&
       for (int q = 0; q < MAXC; ++q) R.cur[r][q] = q == G ? psip[r] : make_double2(0.0, 0.0);
     }
     if ((int)threadIdx.x < G)  // channel offsets of the top columns (read after chain_l's cluster barrier)
-      reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] = gch[threadIdx.x] * 2 * RPT * c.T;
+      reinterpret_cast<int*>(cl_sm + c.rt + 64)[threadIdx.x] = gch[threadIdx.x] * 2 * c.AS;
     bool pairs = G % 2 == 0 && !(E.dbg & 2);  // every pair of tops: consecutive channels, one column pattern
     for (int q = 0; q + 1 < G && pairs; q += 2)
       pairs = gch[q + 1] == gch[q] + 1 && ((E.cl_cshare >> gch[q + 1]) & 1u);
@@ -474,11 +479,12 @@ __device__ __forceinline__ void cll_backward_setup(const LgEngineArgs& E, const 
   for (int kw = 0; kw < E.Kc * 2; ++kw)
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
+      if (c.lr(r) >= c.AS) continue;  // no table entry past the own rows
       const int k = kw >> 1, w = kw & 1;
       const bool ok = c.own(r) && w < E.Wc;
       const long src = ((long)k * E.Wc + w) * c.d;
-      cl_sm[c.acs + kw * RPT * c.T + c.lr(r)] = ok ? E.Ac[src + c.orig(r)] : make_double2(0.0, 0.0);
-      reinterpret_cast<int*>(cl_sm + c.accs)[kw * RPT * c.T + c.lr(r)] =
+      cl_sm[c.acs + kw * c.AS + c.lr(r)] = ok ? E.Ac[src + c.orig(r)] : make_double2(0.0, 0.0);
+      reinterpret_cast<int*>(cl_sm + c.accs)[kw * c.AS + c.lr(r)] =
           ok ? E.cl_accols[src + c.gi(r)] - c.g0 + c.H : c.H + (c.slot(r) ? c.lr(r) : 0);
     }
   cl_sync();

@@ -21,8 +21,15 @@ __host__ __device__ inline int lg_cl_mb_word(int R, int H, int Q, int E, int cma
 // one Taylor term per exchange.  Reduction scratch, 1/(s j) table, two window buffers of cmax
 // columns, staged control rows [acw][2 T] (values, then int columns), then the two exchange
 // mbarriers (one 16-byte word).
+// Entries per staged control row table: one per OWN row (rows past R are never touched), not one per
+// thread slot, so the thread count can exceed R / rpt without growing shared memory.
+__host__ __device__ inline int lg_cll_as(int R, int T, int rpt) {
+  const int r8 = (R + 7) & ~7;
+  return r8 < rpt * T ? r8 : rpt * T;
+}
 __host__ __device__ inline int lg_cll_mb_word(int R, int H, int T, int cmax, int acw, int rpt) {
-  return 16 * 32 + 16 * 16 + 72 + 2 * cmax * (R + 2 * H) + acw * rpt * T + (acw * rpt * T + 3) / 4;
+  const int as = lg_cll_as(R, T, rpt);
+  return 16 * 32 + 16 * 16 + 72 + 2 * cmax * (R + 2 * H) + acw * as + (acw * as + 3) / 4;
 }
 
 // Cost kinds (src/costs.py:49-61)
