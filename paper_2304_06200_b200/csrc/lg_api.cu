@@ -211,7 +211,16 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
         };
         // concurrent item kernel: only when the adjoint sweep fits the GPU at once (its clusters then
         // all start; the item kernel checks that and otherwise exits at once, lg_sweep_cl.cuh bk_may_run)
-        const bool conc = p->n_groups < p->cl_aux_ncl && !std::getenv("LG_CL_SERIAL");
+        // More trajectories than cluster slots (c4: 32 on 7): the adjoint sweep's last wave leaves
+        // slots free (4 of 7 used).  A concurrent item kernel of that many clusters, launched behind the
+        // adjoint sweep, is dispatched once the sweep has no cluster left to issue -- i.e. into those
+        // slots -- and bk_may_run makes a cluster that was placed earlier leave at once (LG_CL_TAIL=0: off).
+        const int tail_free = !ilay && p->cl_aux_ncl > 0 && p->n_groups > p->cl_aux_ncl && p->n_groups % p->cl_aux_ncl
+                                  ? p->cl_aux_ncl - p->n_groups % p->cl_aux_ncl
+                                  : 0;
+        const char* etail = std::getenv("LG_CL_TAIL");
+        const bool tail = tail_free > 0 && !(etail && std::atoi(etail) == 0);
+        const bool conc = (p->n_groups < p->cl_aux_ncl || tail) && !std::getenv("LG_CL_SERIAL");
         if (conc) {
           if (!p->stream2) CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
           if (!p->ev_fork) CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
@@ -223,7 +232,7 @@ int run_sweeps(lg_problem* p, long N, bool grad) {
         if (conc) {
           CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
           E.bk_conc = 1;
-          rc = item_launch((int)std::min<long>(incl, items), p->stream2);
+          rc = item_launch(p->n_groups < p->cl_aux_ncl ? (int)std::min<long>(incl, items) : tail_free, p->stream2);
           E.bk_conc = 0;
           if (rc) return rc;
         }
