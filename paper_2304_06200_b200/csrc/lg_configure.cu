@@ -4,11 +4,11 @@
 
 namespace lgi {
 
-// thread count of the LARGE cluster kernels (lg_sweep_cl_large.cuh: __launch_bounds__(384))
+// thread count of the LARGE cluster kernels (lg_sweep_cl_large.cuh: __launch_bounds__(320))
 static int cll_threads() {
   const char* e = std::getenv("LG_CLL_T");
   const int t = e ? std::atoi(e) : 320;
-  return t >= 64 && t <= 384 && t % 32 == 0 ? t : 320;
+  return t >= 64 && t <= 320 && t % 32 == 0 ? t : 320;
 }
 
 // Reverse Cuthill-McKee renumbering of a symmetric pattern (rows -> neighbour lists).
@@ -266,9 +266,9 @@ bool configure_cl(lg_problem* p, int smem_optin) {
   // three rows per thread at 224 threads (255 registers, 7 warps): 108.8 / 795.3 ms.
   int threads = 32 * ((R + 2 * E + 31) / 32);
   const bool force_large = std::getenv("LG_CL_LARGE") && std::atoi(std::getenv("LG_CL_LARGE")) == 1;
-  // LG_CLL_T=384 (A/B knob): 12 warps = 3 per SM sub-partition instead of 10 warps loading them
-  // 3 / 3 / 2 / 2.  Measured neutral (c4 N' = 400: 791.8 vs 791.5 ms; c3 96.8 vs 97.3 ms): the terms are
-  // paced by the SM-wide shared-memory pipe, not by the fullest sub-partition.
+  // 12 warps (384 threads, 3 per SM sub-partition instead of 3 / 3 / 2 / 2) were measured neutral in
+  // total (c4 N' = 400: 791.8 vs 791.5 ms) and need __launch_bounds__(384), under which ptxas gives the
+  // forward kernel 160 registers and a slower schedule (107 vs 94.5 ms): the kernels stay at 320.
   const int rpt = 2, LT = cll_threads(), lsm = 3;
   if ((!small || force_large) && Q == 1 && p->Wc <= 2 && R <= rpt * LT && !std::getenv("LG_CL_NOLARGE")) {
     const int cstl = cmax | 1;

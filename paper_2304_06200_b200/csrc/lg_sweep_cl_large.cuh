@@ -25,11 +25,9 @@
 #pragma once
 
 // RPT rows per thread at the thread count that gives the register budget they need (R <= RPT T):
-// RPT 2 -> up to 384 threads (12 warps = 3 per SM sub-partition, 168 registers: the register file is
-// split per sub-partition, so 10 warps have the same budget but load the sub-partitions 3 / 3 / 2 / 2),
-// RPT 3 -> 224 threads (7 warps, 255 registers).  The host launches LG_CLL_T threads (default 320; 384
-// measured neutral).
-#define CLL_T(RPT) ((RPT) == 2 ? 384 : 224)
+// RPT 2 -> 320 threads (10 warps, 168 registers: the register file is split per SM sub-partition and two
+// of them hold 3 warps), RPT 3 -> 224 threads (7 warps, 255 registers).  LG_CLL_T launches fewer threads.
+#define CLL_T(RPT) ((RPT) == 2 ? 320 : 224)
 
 namespace {
 
@@ -187,7 +185,11 @@ __device__ __forceinline__ void term_l(const ClL& c, ClLRegs<W, MAXC, RPT>& R, i
   const char* xbuf = reinterpret_cast<const char*>(cl_sm + X);
 #pragma unroll
   for (int rr = 0; rr < RPT; ++rr) {
-    if (!c.slot(rr)) continue;  // thread slots past the CTA's rows (whole warps of them at 384 threads)
+    // thread slots past the CTA's rows skip the term.  The branch also keeps ptxas from interleaving the
+    // two rows' gathers: multi-column terms are register-bound and gain from that (c4 N' = 400 backward
+    // 693 -> 674 ms), a one-column term needs the interleaving to hide its gather latency (forward 94.5 ms
+    // without the branch, 117.5 ms with it), so NC == 1 keeps the unconditional form
+    if (NC > 1 && !c.slot(rr)) continue;
     // FMA chains per column: four (a.x x and a.y (i x) apart) for one or two columns, two for
     // wider terms, whose columns give enough independent chains (and need the registers)
     constexpr bool SPL = NC <= 2;
